@@ -1,0 +1,205 @@
+/*
+ * colbandit_b200.h — C ABI of the B200-native MaxSim / Col-Bandit hot path.
+ *
+ * The reference (arxiv 2602.02827, package ``colbandit`` 0.1.0) is a pure
+ * Python library: it has no FFI of its own. Its hot path sits behind three
+ * Python seams, and every entry point below replaces the
+ * arithmetic behind one of them:
+ *
+ *   cbx_maxsim_scores / cbx_topk_* / cbx_rerank_topk
+ *       replace Similarity.token_scores + MaxSimOracle.row_values/full_score/
+ *       exact_topk (colbandit/oracle.py:57-67, 205-235) for a whole batch of
+ *       queries — the exhaustive scorer (P1).
+ *   cbx_maxsim_cells_f64
+ *       replaces MaxSimOracle.row_values/maxsim (oracle.py:205-220) with
+ *       float64-exact cells, plus math.fsum row scores (oracle.py:222-227);
+ *       backs baselines.full_rerank (baselines.py:89-97).
+ *   cbx_bandit_run
+ *       replaces bandit.run (colbandit/bandit.py:169-350) including the
+ *       ledger / reveal (oracle.py:243-329), the interval arithmetic
+ *       (bounds.py:97-263) and numpy's PCG64 draws — the adaptive loop (P2).
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer unless named host_*; buffers are
+ *     caller-owned; nothing is allocated inside a hot call.
+ *   - Calls are stream-ordered and asynchronous on ``stream`` (a
+ *     cudaStream_t passed as void*; NULL = legacy default stream).
+ *   - Return 0 on success. CBX_EINVAL maps to Python ValueError, CBX_ERANGE
+ *     to IndexError, everything else to RuntimeError; the message is in
+ *     cbx_last_error() (thread-local). No C++ exception crosses the ABI.
+ *   - Reentrant per stream; one process per GPU.
+ */
+#ifndef COLBANDIT_B200_H
+#define COLBANDIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CBX_API __attribute__((visibility("default")))
+#else
+#define CBX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CBX_ABI_VERSION 1
+
+/* status codes */
+#define CBX_OK 0
+#define CBX_EINVAL 1    /* invalid argument       -> ValueError   */
+#define CBX_ERANGE 2    /* index out of range     -> IndexError   */
+#define CBX_ECUDA 3     /* CUDA runtime failure   -> RuntimeError */
+#define CBX_EINTERNAL 4 /* device-side status     -> RuntimeError */
+
+/* element types of token buffers */
+#define CBX_F32 0
+#define CBX_F16 1
+#define CBX_BF16 2
+#define CBX_F64 3
+
+/* scorer path selection for cbx_maxsim_scores */
+#define CBX_PATH_AUTO 0   /* tcgen05 for f16/bf16 with Lq<=128, SIMT otherwise */
+#define CBX_PATH_TC 1     /* TMA + tcgen05 + TMEM dense scorer (f16/bf16)       */
+#define CBX_PATH_SIMT 2   /* CUDA-core scorer, float64 accumulation (any dtype) */
+
+/* explore modes (colbandit/bandit.py:38 EXPLORE_MODES) */
+#define CBX_EPSILON_GREEDY 0
+#define CBX_STATIC_WARMUP 1
+#define CBX_UNIFORM_ROW 2
+
+/* termination codes */
+#define CBX_TERM_SEPARATION 0
+#define CBX_TERM_EXHAUSTION 1
+
+/*
+ * A batch of queries, each with its own candidate documents, CSR-packed.
+ * Query q owns query tokens [q_tok_off[q], q_tok_off[q+1]) of q_tokens and
+ * documents [q_doc_off[q], q_doc_off[q+1]); document i owns doc tokens
+ * [d_tok_off[i], d_tok_off[i+1]) of d_tokens. Token rows are ``dim``
+ * contiguous elements of ``dtype``. Mirrors QueryTokens / DocTokens /
+ * MaxSimOracle(query, docs, similarity) (oracle.py:70-144) for many queries.
+ * The host-side fields (n_*, max_*) describe the device arrays.
+ */
+typedef struct cbx_batch {
+  const void* q_tokens;
+  const int64_t* q_tok_off;   /* [n_queries + 1] */
+  const void* d_tokens;
+  const int64_t* d_tok_off;   /* [n_docs + 1]    */
+  const int64_t* q_doc_off;   /* [n_queries + 1] */
+  int64_t n_queries;
+  int64_t n_docs;
+  int64_t n_q_tokens;
+  int64_t n_d_tokens;
+  int32_t dim;
+  int32_t dtype;              /* CBX_F32 / CBX_F16 / CBX_BF16 / CBX_F64 */
+  int32_t clamp_negative;     /* Similarity.clamp_negative (oracle.py:65-66) */
+  int32_t max_lq;             /* max query tokens over the batch */
+  int64_t max_q_docs;         /* max documents of one query       */
+  int64_t max_q_doc_tokens;   /* max candidate tokens of one query */
+} cbx_batch;
+
+CBX_API int cbx_abi_version(void);
+CBX_API const char* cbx_last_error(void);
+/* SM count and compute capability of the current device. */
+CBX_API int cbx_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---------------------------------------------------------------- P1 */
+/* Scratch needed by cbx_maxsim_scores / cbx_topk_* / cbx_rerank_topk. */
+CBX_API size_t cbx_workspace_bytes(const cbx_batch* b, int k);
+
+/* Dense MaxSim score of every candidate: scores[i] = sum_t max_j <e_ij, q_t>
+ * (float32 accumulate on the tcgen05 path, float64 then rounded on SIMT). */
+CBX_API int cbx_maxsim_scores(const cbx_batch* b, float* scores, int path,
+                      void* workspace, size_t ws_bytes, void* stream);
+
+/* Per-query Top-K by (-score, local index): ties to the lower index like
+ * np.lexsort((arange(N), -S)) (oracle.py:229-235). k must be <= 8192 and
+ * <= every query's pool size. topk_idx holds query-local doc indices. */
+CBX_API int cbx_topk_f32(const float* scores, const int64_t* q_doc_off, int64_t n_queries,
+                 int64_t max_q_docs, int k, int32_t* topk_idx, float* topk_val,
+                 void* workspace, size_t ws_bytes, void* stream);
+CBX_API int cbx_topk_f64(const double* scores, const int64_t* q_doc_off, int64_t n_queries,
+                 int64_t max_q_docs, int k, int32_t* topk_idx, double* topk_val,
+                 void* workspace, size_t ws_bytes, void* stream);
+
+/* Scores + Top-K in one stream-ordered call (the exhaustive reranker). */
+CBX_API int cbx_rerank_topk(const cbx_batch* b, int k, int path, float* scores,
+                    int32_t* topk_idx, float* topk_val,
+                    void* workspace, size_t ws_bytes, void* stream);
+
+/* float64-exact cells: cells[i * ld + t] = max_j <e_ij, q_t> (clamped if
+ * requested) for every doc i of the batch, t < Lq of its query; optional
+ * scores_f64[i] = exactly rounded sum of the row (CPython math.fsum). */
+CBX_API int cbx_maxsim_cells_f64(const cbx_batch* b, double* cells, int64_t ld,
+                         double* scores_f64, void* stream);
+
+/* ---------------------------------------------------------------- P2 */
+/* numpy PCG64 bit-generator state (np.random.default_rng(seed)
+ * .bit_generator.state): 128-bit state and increment plus the buffered
+ * 32-bit half. */
+typedef struct cbx_pcg64 {
+  uint64_t state_hi, state_lo;
+  uint64_t inc_hi, inc_lo;
+  uint32_t has_uint32;
+  uint32_t uinteger;
+} cbx_pcg64;
+
+/* One bandit run (BanditConfig, colbandit/bandit.py:40-76). log_term is
+ * RadiusConfig.log_term(N, T) evaluated on the host with math.log
+ * (bounds.py:138-143). For CBX_STATIC_WARMUP the host draws the warm-up
+ * cells with numpy's Generator.choice and passes them (and the generator
+ * state after that draw) in warm_cells / rng. */
+typedef struct cbx_bandit_run_desc {
+  int64_t query;          /* query index in the batch (token source)          */
+  int64_t doc_begin;      /* first document (global index) of the pool        */
+  int32_t n_docs;         /* pool size N                                      */
+  int32_t k;              /* Top-K target (1 <= k <= N; k == 0 handled on host)*/
+  int32_t explore_mode;   /* CBX_EPSILON_GREEDY / CBX_STATIC_WARMUP / CBX_UNIFORM_ROW */
+  int32_t n_warm;         /* static warm-up cell count                        */
+  int64_t warm_off;       /* offset of this run's cells in warm_cells         */
+  double alpha_ef;
+  double epsilon;
+  double log_term;
+  int64_t bounds_off;     /* element offset of this run's (N x T) lo/hi block, -1 = uniform */
+  double lo_uniform;      /* generic bounds when bounds_off < 0 (bounds.py:177-180) */
+  double hi_uniform;
+  int64_t trace_off;      /* offset of this run's trace slots                 */
+  int64_t trace_cap;      /* capacity (>= N*T is always enough)               */
+  int64_t state_off;      /* offset (in rows) of this run's per-row state     */
+  cbx_pcg64 rng;
+} cbx_bandit_run_desc;
+
+typedef struct cbx_bandit_out {
+  int64_t n_reveals;
+  int32_t iterations;
+  int32_t terminated_by;  /* CBX_TERM_* */
+  int32_t status;         /* 0 ok; nonzero = device-detected error (see cbx_last_error) */
+  int32_t pad;
+} cbx_bandit_out;
+
+/* Cell source: either token embeddings (cells computed on demand in float64
+ * from the batch — MaxSimOracle(query, docs)) or a precomputed float64
+ * matrix (MaxSimOracle.from_matrix, oracle.py:146-176): cell (i, t) of run r
+ * at matrix[(doc_begin + i) * ld_matrix + t]. */
+CBX_API size_t cbx_bandit_state_bytes(int64_t total_rows, int32_t max_t);
+
+CBX_API int cbx_bandit_run(const cbx_batch* b,              /* token source or NULL   */
+                   const double* matrix, int64_t ld_matrix, int32_t n_cols,
+                   const cbx_bandit_run_desc* runs, /* device array [n_runs]  */
+                   int64_t n_runs,
+                   const double* bounds_lo, const double* bounds_hi,
+                   const int32_t* warm_cells,       /* flat cell ids (i*T+t)  */
+                   void* row_state, size_t state_bytes,
+                   int32_t* topk,                   /* [n_runs * max_k]       */
+                   int32_t max_k,
+                   int32_t* trace_i, int32_t* trace_t, double* trace_v,
+                   cbx_bandit_out* out,             /* [n_runs]               */
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COLBANDIT_B200_H */

@@ -1,0 +1,291 @@
+"""Device-resident CSR batches and the batched P1 entry points.
+
+A :class:`TokenBatch` is many ``MaxSimOracle(query, docs)`` instances
+(colbandit/oracle.py:107-144) packed into five device arrays: query tokens,
+query-token offsets, document tokens, document-token offsets and per-query
+document ranges. Tokens stay in their storage dtype (fp16 / bf16 / fp32 /
+fp64) — the reference's float64 upcast (validation.py:14) happens implicitly
+inside the kernels, which accumulate exact products.
+
+Entry points (all stream-ordered on torch's current stream):
+
+* :func:`maxsim_scores`  — dense MaxSim score of every candidate (P1 kernel)
+* :func:`rerank_topk`    — scores + per-query Top-K (the exhaustive reranker)
+* :func:`exact_cells`    — float64-exact cell matrix + fsum row scores
+* :func:`topk`           — per-query Top-K of a score vector
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+
+__all__ = ["TokenBatch", "maxsim_scores", "rerank_topk", "exact_cells", "topk", "dtype_code"]
+
+_PATHS = {"auto": _lib.CBX_PATH_AUTO, "tc": _lib.CBX_PATH_TC, "tcgen05": _lib.CBX_PATH_TC, "simt": _lib.CBX_PATH_SIMT}
+
+
+def dtype_code(tdtype) -> int:
+    import torch
+
+    codes = {torch.float32: _lib.CBX_F32, torch.float16: _lib.CBX_F16, torch.bfloat16: _lib.CBX_BF16,
+             torch.float64: _lib.CBX_F64}
+    if tdtype not in codes:
+        raise ValueError(f"unsupported token dtype {tdtype}; expected float16, bfloat16, float32 or float64")
+    return codes[tdtype]
+
+
+def to_torch_tokens(arr, dtype: str | None = None):
+    """numpy / torch token matrix -> CPU torch tensor in its storage dtype.
+
+    numpy uint16 arrays are bf16 bit patterns and need ``dtype="bf16"``.
+    """
+    import torch
+
+    if isinstance(arr, torch.Tensor):
+        return arr
+    a = np.ascontiguousarray(arr)
+    if dtype == "bf16" or (a.dtype == np.uint16 and dtype is None):
+        if a.dtype != np.uint16:
+            raise ValueError("bf16 tokens must be given as uint16 bit patterns or a torch.bfloat16 tensor")
+        return torch.from_numpy(a.view(np.int16)).view(torch.bfloat16)
+    if a.dtype not in (np.float16, np.float32, np.float64):
+        a = a.astype(np.float64)
+    return torch.from_numpy(a)
+
+
+@dataclass
+class TokenBatch:
+    q_tokens: "object"    # torch [n_q_tokens, dim]
+    q_tok_off: "object"   # torch int64 [n_queries + 1]
+    d_tokens: "object"    # torch [n_d_tokens, dim]
+    d_tok_off: "object"   # torch int64 [n_docs + 1]
+    q_doc_off: "object"   # torch int64 [n_queries + 1]
+    clamp_negative: bool = False
+    max_lq: int = 0
+    max_q_docs: int = 0
+    max_q_doc_tokens: int = 0
+
+    # -------------------------------------------------------------- construction
+    @classmethod
+    def from_device(cls, q_tokens, q_tok_off, d_tokens, d_tok_off, q_doc_off, clamp_negative=False,
+                    host_offsets=None) -> "TokenBatch":
+        """Wrap device tensors; host copies of the offsets (given or fetched) size the launch."""
+        if host_offsets is None:
+            host_offsets = (q_tok_off.cpu().numpy(), d_tok_off.cpu().numpy(), q_doc_off.cpu().numpy())
+        qo, do, qd = (np.asarray(x, dtype=np.int64) for x in host_offsets)
+        lq = np.diff(qo)
+        ndocs = np.diff(qd)
+        qtoks = do[qd[1:]] - do[qd[:-1]] if len(qd) > 1 else np.zeros(0, np.int64)
+        b = cls(q_tokens, q_tok_off, d_tokens, d_tok_off, q_doc_off, bool(clamp_negative),
+                int(lq.max()) if len(lq) else 0, int(ndocs.max()) if len(ndocs) else 0,
+                int(qtoks.max()) if len(qtoks) else 0)
+        b._validate()
+        return b
+
+    @classmethod
+    def from_host(cls, queries: Sequence, docs: Sequence[Sequence], dtype: str | None = None,
+                  clamp_negative: bool = False, device=None) -> "TokenBatch":
+        """Pack host queries and per-query doc lists (numpy or torch) into one device batch."""
+        torch = _lib.require_cuda()
+        if len(queries) != len(docs):
+            raise ValueError("one candidate list per query is required")
+        qt = [to_torch_tokens(q, dtype) for q in queries]
+        dt = [[to_torch_tokens(d, dtype) for d in dl] for dl in docs]
+        flat_docs = [d for dl in dt for d in dl]
+        tdt = qt[0].dtype if qt else torch.float32
+        for t in qt + flat_docs:
+            if t.dtype != tdt:
+                raise ValueError("all token matrices of a batch must share one dtype")
+        qo = np.zeros(len(qt) + 1, np.int64)
+        np.cumsum([t.shape[0] for t in qt], out=qo[1:])
+        do = np.zeros(len(flat_docs) + 1, np.int64)
+        np.cumsum([t.shape[0] for t in flat_docs], out=do[1:])
+        qd = np.zeros(len(dt) + 1, np.int64)
+        np.cumsum([len(dl) for dl in dt], out=qd[1:])
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        dim = qt[0].shape[1] if qt else 1
+        qcat = torch.cat(qt).contiguous() if qt else torch.zeros((0, dim), dtype=tdt)
+        dcat = torch.cat(flat_docs).contiguous() if flat_docs else torch.zeros((0, dim), dtype=tdt)
+        return cls.from_device(
+            qcat.to(device, non_blocking=False), torch.from_numpy(qo).to(device), dcat.to(device),
+            torch.from_numpy(do).to(device), torch.from_numpy(qd).to(device), clamp_negative,
+            host_offsets=(qo, do, qd))
+
+    def _validate(self) -> None:
+        import torch
+
+        for name in ("q_tokens", "d_tokens"):
+            t = getattr(self, name)
+            if not t.is_cuda:
+                raise ValueError(f"{name} must live on a CUDA device")
+            if t.dim() != 2:
+                raise ValueError(f"{name} must be 2-D (tokens x dim)")
+            if not t.is_contiguous():
+                raise ValueError(f"{name} must be contiguous")
+            if t.data_ptr() % 16:
+                raise ValueError(f"{name} must be 16-byte aligned")
+        if self.q_tokens.dtype != self.d_tokens.dtype:
+            raise ValueError("query and document tokens must share one dtype")
+        if self.q_tokens.shape[1] != self.d_tokens.shape[1]:
+            raise ValueError(
+                f"doc embedding dim {self.d_tokens.shape[1]} does not match query dim {self.q_tokens.shape[1]}")
+        for name in ("q_tok_off", "d_tok_off", "q_doc_off"):
+            t = getattr(self, name)
+            if t.dtype != torch.int64 or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous int64 CUDA tensor")
+        dtype_code(self.q_tokens.dtype)
+
+    # -------------------------------------------------------------- properties
+    @property
+    def n_queries(self) -> int:
+        return self.q_doc_off.shape[0] - 1
+
+    @property
+    def n_docs(self) -> int:
+        return self.d_tok_off.shape[0] - 1
+
+    @property
+    def dim(self) -> int:
+        return int(self.q_tokens.shape[1])
+
+    def struct(self) -> _lib.CbxBatch:
+        s = _lib.CbxBatch()
+        s.q_tokens = self.q_tokens.data_ptr()
+        s.q_tok_off = self.q_tok_off.data_ptr()
+        s.d_tokens = self.d_tokens.data_ptr()
+        s.d_tok_off = self.d_tok_off.data_ptr()
+        s.q_doc_off = self.q_doc_off.data_ptr()
+        s.n_queries = self.n_queries
+        s.n_docs = self.n_docs
+        s.n_q_tokens = int(self.q_tokens.shape[0])
+        s.n_d_tokens = int(self.d_tokens.shape[0])
+        s.dim = self.dim
+        s.dtype = dtype_code(self.q_tokens.dtype)
+        s.clamp_negative = 1 if self.clamp_negative else 0
+        s.max_lq = self.max_lq
+        s.max_q_docs = self.max_q_docs
+        s.max_q_doc_tokens = self.max_q_doc_tokens
+        return s
+
+
+def _stream_ptr():
+    import torch
+
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _workspace(nbytes: int):
+    import torch
+
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device="cuda")
+
+
+def maxsim_scores(batch: TokenBatch, path: str = "auto", out=None):
+    """float32 MaxSim score of every candidate document of the batch."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    if path not in _PATHS:
+        raise ValueError(f"path must be one of {sorted(_PATHS)}, got {path!r}")
+    if out is None:
+        out = torch.empty(batch.n_docs, dtype=torch.float32, device=batch.d_tokens.device)
+    s = batch.struct()
+    _lib.check(lib.cbx_maxsim_scores(ctypes.byref(s), out.data_ptr(), _PATHS[path], None, 0, _stream_ptr()),
+               "maxsim_scores")
+    return out
+
+
+def topk(scores, q_doc_off, k: int, max_q_docs: int):
+    """Per-query Top-K (query-local indices, values) of float32 or float64 scores."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    nq = q_doc_off.shape[0] - 1
+    if k < 0:
+        raise ValueError(f"k must be non-negative, got {k}")
+    idx = torch.empty((nq, k), dtype=torch.int32, device=scores.device)
+    val = torch.empty((nq, k), dtype=scores.dtype, device=scores.device)
+    s = _lib.CbxBatch()
+    s.n_queries, s.max_q_docs = nq, max_q_docs
+    ws = _workspace(lib.cbx_workspace_bytes(ctypes.byref(s), k))
+    fn = lib.cbx_topk_f32 if scores.dtype == torch.float32 else lib.cbx_topk_f64
+    _lib.check(fn(scores.data_ptr(), q_doc_off.data_ptr(), nq, max_q_docs, k, idx.data_ptr(), val.data_ptr(),
+                  ws.data_ptr(), ws.numel(), _stream_ptr()), "topk")
+    return idx, val
+
+
+def rerank_topk(batch: TokenBatch, k: int, path: str = "auto"):
+    """Exhaustive reranking: (Top-K local indices [nq, k], Top-K scores, all scores)."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    if path not in _PATHS:
+        raise ValueError(f"path must be one of {sorted(_PATHS)}, got {path!r}")
+    nq = batch.n_queries
+    scores = torch.empty(batch.n_docs, dtype=torch.float32, device=batch.d_tokens.device)
+    idx = torch.empty((nq, k), dtype=torch.int32, device=scores.device)
+    val = torch.empty((nq, k), dtype=torch.float32, device=scores.device)
+    s = batch.struct()
+    ws = _workspace(lib.cbx_workspace_bytes(ctypes.byref(s), k))
+    _lib.check(lib.cbx_rerank_topk(ctypes.byref(s), k, _PATHS[path], scores.data_ptr(), idx.data_ptr(),
+                                   val.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr()), "rerank_topk")
+    return idx, val, scores
+
+
+def exact_cells(batch: TokenBatch, with_scores: bool = True):
+    """float64-exact cells [n_docs, max_lq] (NaN beyond each query's Lq) and fsum row scores."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    ld = max(batch.max_lq, 1)
+    cells = torch.full((batch.n_docs, ld), float("nan"), dtype=torch.float64, device=batch.d_tokens.device)
+    scores = torch.empty(batch.n_docs, dtype=torch.float64, device=cells.device) if with_scores else None
+    s = batch.struct()
+    _lib.check(lib.cbx_maxsim_cells_f64(ctypes.byref(s), cells.data_ptr(), ld,
+                                        scores.data_ptr() if scores is not None else None, _stream_ptr()),
+               "exact_cells")
+    return cells, scores
+
+
+class HostBatch:
+    """A TokenBatch's arrays in pinned host memory plus reusable device buffers.
+
+    ``rerank_topk_host`` is the end-to-end public call: host->device copies of
+    the step's inputs, the exhaustive reranker, device->host copy of the
+    per-query Top-K — all stream-ordered on one stream.
+    """
+
+    def __init__(self, q_tokens, q_tok_off, d_tokens, d_tok_off, q_doc_off, clamp_negative=False):
+        torch = _lib.require_cuda()
+        pin = lambda t: t.contiguous().pin_memory()  # noqa: E731
+        self.host = [pin(t) for t in (q_tokens, q_tok_off, d_tokens, d_tok_off, q_doc_off)]
+        self.dev = [torch.empty_like(t, device="cuda") for t in self.host]
+        self.clamp_negative = clamp_negative
+        offs = [t.numpy() for t in self.host[1::2]]
+        self.batch = TokenBatch.from_device(*self.dev, clamp_negative=clamp_negative,
+                                            host_offsets=(offs[0], offs[1], self.host[4].numpy()))
+
+    @classmethod
+    def from_device_batch(cls, b: TokenBatch) -> "HostBatch":
+        return cls(b.q_tokens.cpu(), b.q_tok_off.cpu(), b.d_tokens.cpu(), b.d_tok_off.cpu(), b.q_doc_off.cpu(),
+                   b.clamp_negative)
+
+    @property
+    def h2d_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self.host)
+
+
+def rerank_topk_host(hb: HostBatch, k: int, path: str = "auto", out=None):
+    """End-to-end exhaustive reranking from pinned host buffers to host Top-K."""
+    torch = _lib.require_cuda()
+    for h, d in zip(hb.host, hb.dev):
+        d.copy_(h, non_blocking=True)
+    idx, val, _ = rerank_topk(hb.batch, k, path)
+    if out is None:
+        out = (torch.empty(idx.shape, dtype=idx.dtype).pin_memory(),
+               torch.empty(val.shape, dtype=val.dtype).pin_memory())
+    out[0].copy_(idx, non_blocking=True)
+    out[1].copy_(val, non_blocking=True)
+    return out

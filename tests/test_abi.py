@@ -1,0 +1,65 @@
+"""CPU-side checks of the C ABI: the library loads and exports every declared symbol."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT, cuda_available
+from paper_2602_02827_b200 import _lib
+
+HEADER = os.path.join(ROOT, "include", "colbandit_b200.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^CBX_API\s+[\w\s\*]+?\b(cbx_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_header_declares_the_entry_points():
+    syms = declared_symbols()
+    for name in ("cbx_maxsim_scores", "cbx_topk_f32", "cbx_rerank_topk", "cbx_maxsim_cells_f64",
+                 "cbx_bandit_run", "cbx_last_error", "cbx_abi_version"):
+        assert name in syms
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
+    assert set(_lib.SIGNATURES) == set(declared_symbols())
+    assert lib.cbx_abi_version() == 1
+
+
+def test_struct_layouts_match_the_header():
+    # sizes follow the C layout (natural alignment, 64-bit)
+    assert ctypes.sizeof(_lib.CbxBatch) == 5 * 8 + 4 * 8 + 4 * 4 + 2 * 8
+    assert ctypes.sizeof(_lib.CbxPcg64) == 4 * 8 + 2 * 4
+    assert ctypes.sizeof(_lib.CbxBanditOut) == 8 + 4 * 4
+
+
+def test_library_is_sm100a_only():
+    path = _lib.LIB_PATH
+    data = open(path, "rb").read()
+    assert b"sm_100a" in data or b"sm_100" in data
+
+
+@pytest.mark.skipif(cuda_available(), reason="checks the no-GPU failure mode")
+def test_product_path_fails_loudly_without_a_gpu():
+    from paper_2602_02827_b200.batch import TokenBatch
+
+    import numpy as np
+
+    with pytest.raises(RuntimeError, match="CUDA device"):
+        TokenBatch.from_host([np.ones((2, 8), np.float16)], [[np.ones((3, 8), np.float16)]])
+
+
+def test_error_mapping():
+    with pytest.raises(ValueError):
+        _lib.check(_lib.CBX_EINVAL)
+    with pytest.raises(IndexError):
+        _lib.check(_lib.CBX_ERANGE)
+    with pytest.raises(RuntimeError):
+        _lib.check(_lib.CBX_EINTERNAL)
