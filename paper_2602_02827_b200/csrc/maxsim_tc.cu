@@ -41,13 +41,15 @@ struct TcParams {
   const int64_t* d_tok_off;
   const int64_t* q_doc_off;
   float* scores;
-  int64_t n_chunks;      // n_queries * chunks_per_query
-  int64_t chunks_per_query;
-  int64_t chunk_tokens;  // T
+  int64_t n_queries;
+  int64_t n_docs;
+  int64_t n_tokens;      // total document tokens (partitioned evenly over the CTAs)
   uint32_t idesc;
   int32_t tile_n;
   int32_t kblocks;       // ceil(dim / 64)
-  int32_t lqp;           // query rows staged per slot (max Lq rounded up to 8)
+  int32_t lqp;           // query rows per replica (max Lq rounded up to 32)
+  int32_t nq;            // TMEM lane quadrants per replica (lqp / 32)
+  int32_t rep;           // query replicas in the 128-row A operand (4 / nq, 1 if nq == 3)
   int32_t stages;
   int32_t clamp_negative;
   uint32_t q_slot_bytes;
@@ -73,23 +75,42 @@ __device__ __forceinline__ int64_t lower_bound_start(const int64_t* __restrict__
   return lo;
 }
 
-__device__ __forceinline__ bool decode_chunk(const TcParams& p, int64_t g, ChunkInfo& c) {
-  int64_t q = g / p.chunks_per_query;
-  int64_t k = g - q * p.chunks_per_query;
-  int64_t db = __ldg(p.q_doc_off + q), de = __ldg(p.q_doc_off + q + 1);
-  if (db >= de) return false;
-  int64_t qs = __ldg(p.d_tok_off + db);
-  int64_t x0 = qs + k * p.chunk_tokens, x1 = x0 + p.chunk_tokens;
-  c.doc0 = lower_bound_start(p.d_tok_off, db, de, x0);
-  c.doc1 = lower_bound_start(p.d_tok_off, c.doc0, de, x1);
-  if (c.doc0 >= c.doc1) return false;
-  c.cs = __ldg(p.d_tok_off + c.doc0);
-  c.ce = __ldg(p.d_tok_off + c.doc1);
-  c.q_tok0 = __ldg(p.q_tok_off + q);
-  c.lq = (int32_t)(__ldg(p.q_tok_off + q + 1) - c.q_tok0);
-  c.ntiles = (int32_t)((c.ce - c.cs + p.tile_n - 1) / p.tile_n);
-  return true;
-}
+// Static balanced partition: CTA b owns the documents whose first token lies in
+// [b * n_tokens / G, (b + 1) * n_tokens / G); its "chunks" are that document
+// range cut at query boundaries, visited in order. Every role walks the same
+// sequence, so no scheduling state is exchanged.
+struct ChunkCursor {
+  int64_t doc, doc_hi, q;
+  __device__ __forceinline__ void init(const TcParams& p) {
+    const int64_t G = gridDim.x, b = blockIdx.x;
+    const int64_t x0 = (int64_t)((__int128)p.n_tokens * b / G);
+    const int64_t x1 = (int64_t)((__int128)p.n_tokens * (b + 1) / G);
+    doc = lower_bound_start(p.d_tok_off, 0, p.n_docs, x0);
+    doc_hi = lower_bound_start(p.d_tok_off, doc, p.n_docs, x1);
+    // query owning `doc`: last q with q_doc_off[q] <= doc
+    int64_t lo = 0, hi = p.n_queries;
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (__ldg(p.q_doc_off + mid) <= doc) lo = mid;
+      else hi = mid;
+    }
+    q = lo;
+  }
+  __device__ __forceinline__ bool next(const TcParams& p, ChunkInfo& c) {
+    if (doc >= doc_hi) return false;
+    int64_t qe;
+    while ((qe = __ldg(p.q_doc_off + q + 1)) <= doc) ++q;
+    c.doc0 = doc;
+    c.doc1 = qe < doc_hi ? qe : doc_hi;
+    doc = c.doc1;
+    c.cs = __ldg(p.d_tok_off + c.doc0);
+    c.ce = __ldg(p.d_tok_off + c.doc1);
+    c.q_tok0 = __ldg(p.q_tok_off + q);
+    c.lq = (int32_t)(__ldg(p.q_tok_off + q + 1) - c.q_tok0);
+    c.ntiles = (int32_t)((c.ce - c.cs + p.tile_n - 1) / p.tile_n);
+    return true;
+  }
+};
 
 __device__ __forceinline__ float warp_sum(float x) {
 #pragma unroll
@@ -97,22 +118,51 @@ __device__ __forceinline__ float warp_sum(float x) {
   return x;
 }
 
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// max of 32 register values (FMNMX3 tree)
+__device__ __forceinline__ float max32(const float (&v)[32]) {
+  float a[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) a[i] = fmax3f(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+  a[10] = fmaxf(v[30], v[31]);
+  float b0 = fmax3f(a[0], a[1], a[2]), b1 = fmax3f(a[3], a[4], a[5]), b2 = fmax3f(a[6], a[7], a[8]);
+  float b3 = fmaxf(a[9], a[10]);
+  return fmaxf(fmax3f(b0, b1, b2), b3);
+}
+
+// max of v[j] for s <= j < e (s, e warp-uniform), starting from m
+__device__ __forceinline__ float masked_max(const float (&v)[32], int s, int e, float m) {
+  const uint32_t bits = (e >= 32 ? 0xFFFFFFFFu : ((1u << e) - 1u)) & ~((1u << s) - 1u);
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (bits & (1u << j)) m = fmaxf(m, v[j]);
+  return m;
+}
+
 __global__ void __launch_bounds__(TC_THREADS, 1)
     maxsim_tc_kernel(const __grid_constant__ CUtensorMap tmap_d, const __grid_constant__ CUtensorMap tmap_q,
                      const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* q_slots = smem;                                   // 2 x q_slot_bytes
-  uint8_t* stages = smem + 2 * p.q_slot_bytes;               // stages x stage_bytes
+  uint8_t* q_slot = smem;                                    // kblocks x (128 rows x 128 B)
+  uint8_t* stages = smem + p.q_slot_bytes;                   // stages x stage_bytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)p.stages * p.stage_bytes);
-  uint64_t* full = bars;                                     // [stages]
-  uint64_t* empty = bars + TC_MAX_STAGES;                    // [stages]
-  uint64_t* qfull = bars + 2 * TC_MAX_STAGES;                // [2]
-  uint64_t* qempty = qfull + 2;                              // [2]
-  uint64_t* tfull = qempty + 2;                              // [4]
+  uint64_t* full = bars;                                     // [TC_MAX_STAGES]
+  uint64_t* empty = bars + TC_MAX_STAGES;                    // [TC_MAX_STAGES]
+  uint64_t* qfull = bars + 2 * TC_MAX_STAGES;                // [1]
+  uint64_t* qempty = qfull + 1;                              // [1]
+  uint64_t* tfull = qempty + 1;                              // [4]
   uint64_t* tempty = tfull + TC_ACC_BUFS;                    // [4]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + TC_ACC_BUFS);
-  float* part = reinterpret_cast<float*>(bars + 64);         // [2][4][TC_MAX_TILE_N]
+  uint64_t* cfull = tempty + TC_ACC_BUFS;                    // [4] carry published
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cfull + TC_ACC_BUFS);
+  float* carry = reinterpret_cast<float*>(bars + 64);        // [4 slots][4 warps][32]
+  float* part = carry + 4 * 4 * 32;                          // [2 parity][4 quads][TC_MAX_TILE_N]
+  int64_t* part_doc = reinterpret_cast<int64_t*>(part + 2 * 4 * TC_MAX_TILE_N);  // [2][2 groups][TC_MAX_TILE_N]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -122,13 +172,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      ptx::mbar_init(&qfull[s], 1);
-      ptx::mbar_init(&qempty[s], 1);
-    }
+    ptx::mbar_init(qfull, 1);
+    ptx::mbar_init(qempty, 1);
     for (int s = 0; s < TC_ACC_BUFS; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], 4);
+      ptx::mbar_init(&tempty[s], p.nq);
+      ptx::mbar_init(&cfull[s], p.nq);
     }
     ptx::fence_mbarrier_init();
   }
@@ -145,17 +194,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0, qs = 0, qphase = 0;
+      uint32_t stage = 0, phase = 0, qphase = 0;
       const uint64_t pol = ptx::policy_evict_first();
-      for (int64_t g = blockIdx.x; g < p.n_chunks; g += gridDim.x) {
-        ChunkInfo c;
-        if (!decode_chunk(p, g, c)) continue;
-        ptx::mbar_wait(&qempty[qs], qphase ^ 1);
-        ptx::mbar_arrive_expect_tx(&qfull[qs], p.q_slot_bytes);
-        for (int kb = 0; kb < p.kblocks; ++kb)
-          ptx::tma_load_2d(q_slots + qs * p.q_slot_bytes + kb * p.lqp * 128, &tmap_q, &qfull[qs], kb * 64,
-                           (int32_t)c.q_tok0);
-        if (++qs == 2) { qs = 0; qphase ^= 1; }
+      ChunkCursor cur;
+      cur.init(p);
+      ChunkInfo c;
+      while (cur.next(p, c)) {
+        // one query slot: reload only after every MMA of the previous chunk retired
+        ptx::mbar_wait(qempty, qphase ^ 1);
+        ptx::mbar_arrive_expect_tx(qfull, (uint32_t)(p.rep * p.kblocks * p.lqp * 128));
+        for (int g = 0; g < p.rep; ++g)
+          for (int kb = 0; kb < p.kblocks; ++kb)
+            ptx::tma_load_2d(q_slot + kb * 16384 + g * p.lqp * 128, &tmap_q, qfull, kb * 64, (int32_t)c.q_tok0);
+        qphase ^= 1;
         for (int t = 0; t < c.ntiles; ++t) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[stage], p.stage_bytes);
@@ -170,15 +221,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0, qs = 0, qphase = 0, acc = 0, aphase = 0;
-      for (int64_t g = blockIdx.x; g < p.n_chunks; g += gridDim.x) {
-        ChunkInfo c;
-        if (!decode_chunk(p, g, c)) continue;
-        ptx::mbar_wait(&qfull[qs], qphase);
+      uint32_t stage = 0, phase = 0, qphase = 0, tg = 0;
+      ChunkCursor cur;
+      cur.init(p);
+      ChunkInfo c;
+      const uint32_t q_addr = ptx::smem_u32(q_slot);
+      while (cur.next(p, c)) {
+        ptx::mbar_wait(qfull, qphase);
+        qphase ^= 1;
         ptx::tc_fence_after();
-        const uint32_t q_addr = ptx::smem_u32(q_slots + qs * p.q_slot_bytes);
-        for (int t = 0; t < c.ntiles; ++t) {
-          ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+        for (int t = 0; t < c.ntiles; ++t, ++tg) {
+          const uint32_t acc = tg & (TC_ACC_BUFS - 1);
+          ptx::mbar_wait(&tempty[acc], ((tg >> 2) & 1) ^ 1);
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t b_addr = ptx::smem_u32(stages + (size_t)stage * p.stage_bytes);
@@ -186,7 +240,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int kb = 0; kb < p.kblocks; ++kb) {
 #pragma unroll
             for (int k4 = 0; k4 < 4; ++k4) {
-              uint64_t ad = ptx::smem_desc_sw128(q_addr + kb * p.lqp * 128 + k4 * 32);
+              uint64_t ad = ptx::smem_desc_sw128(q_addr + kb * 16384 + k4 * 32);
               uint64_t bd = ptx::smem_desc_sw128(b_addr + kb * p.tile_n * 128 + k4 * 32);
               ptx::tc_mma_f16(d_tmem, ad, bd, p.idesc, (kb | k4) != 0);
             }
@@ -194,107 +248,155 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           ptx::tc_commit(&empty[stage]);
           ptx::tc_commit(&tfull[acc]);
           if (++stage == (uint32_t)p.stages) { stage = 0; phase ^= 1; }
-          if (++acc == TC_ACC_BUFS) { acc = 0; aphase ^= 1; }
         }
-        ptx::tc_commit(&qempty[qs]);
-        if (++qs == 2) { qs = 0; qphase ^= 1; }
+        ptx::tc_commit(qempty);
       }
     }
   } else if (warp >= TC_EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - TC_EPI_WARP0;  // TMEM lane quadrant
-    uint32_t acc = 0, aphase = 0, tile_parity = 0;
-    const float init = p.clamp_negative ? 0.0f : -INFINITY;
-    for (int64_t g = blockIdx.x; g < p.n_chunks; g += gridDim.x) {
+    // The query sits in the A operand `rep` times (rows g*lqp ...), so every
+    // TMEM lane group holds the same scores; group g (nq warps = nq lane
+    // quadrants) takes the CTA's tiles with index % rep == g. A document
+    // spanning tiles is stitched through a carry chain: each tile publishes
+    // the running max of the document open at its end (slot tg % 4), the
+    // next tile merges it into its head segment.
+    const int quad = warp - TC_EPI_WARP0;
+    const int nq = p.nq, rep = p.rep;
+    const int grp = quad / nq, wig = quad - grp * nq;
+    if (grp < rep) {
+      const float init = p.clamp_negative ? 0.0f : -INFINITY;
+      const uint32_t tmem_lane = (uint32_t)(quad * 32) << 16;
+      uint32_t tg = 0, pb = 0;
+      ChunkCursor cursor;
+      cursor.init(p);
       ChunkInfo c;
-      if (!decode_chunk(p, g, c)) continue;
-      const int nact = (c.lq + 31) >> 5;
-      const bool active = ew < nact;
-      const bool lane_valid = ew * 32 + lane < c.lq;
-      float cur = init;
-      // window of 32 document end offsets, one per lane
-      int64_t win = c.doc0;
-      int64_t ends = (win + lane < c.doc1) ? __ldg(p.d_tok_off + win + 1 + lane) : INT64_MAX;
-      int64_t doc = c.doc0;
-      int64_t doc_end = __shfl_sync(0xffffffffu, ends, 0);
-      for (int t = 0; t < c.ntiles; ++t) {
-        ptx::mbar_wait(&tfull[acc], aphase);
-        ptx::tc_fence_after();
-        const int64_t tbase = c.cs + (int64_t)t * p.tile_n;
-        const int ncols = (int)(c.ce - tbase < p.tile_n ? c.ce - tbase : p.tile_n);
-        float v[TC_MAX_TILE_N / 32][32];
-        if (active) {
-          const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * TC_MAX_TILE_N;
+      while (cursor.next(p, c)) {
+        const bool lane_valid = wig * 32 + lane < c.lq;
+        // window of document end offsets: ends[lane] = end of doc (win + lane)
+        int64_t win = c.doc0;
+        int64_t ends = (win + lane < c.doc1) ? __ldg(p.d_tok_off + win + 1 + lane) : INT64_MAX;
+        int64_t ends_nx = (win + 32 + lane < c.doc1) ? __ldg(p.d_tok_off + win + 33 + lane) : INT64_MAX;
+        int64_t doc = c.doc0;
+        int64_t prev_end = c.cs;
+        for (int t = 0; t < c.ntiles; ++t, ++tg) {
+          if ((int)(tg % (uint32_t)rep) != grp) continue;
+          const uint32_t acc = tg & (TC_ACC_BUFS - 1);
+          ptx::mbar_wait(&tfull[acc], (tg >> 2) & 1);
+          ptx::tc_fence_after();
+          const int64_t tb = c.cs + (int64_t)t * p.tile_n;
+          const int ncols = (int)(c.ce - tb < p.tile_n ? c.ce - tb : p.tile_n);
+          float v[TC_MAX_TILE_N / 32][32];
+          const uint32_t taddr = tmem_base + tmem_lane + acc * TC_MAX_TILE_N;
 #pragma unroll
           for (int b = 0; b < TC_MAX_TILE_N / 32; ++b)
             if (b * 32 < ncols) ptx::tmem_ld_32x32b_x32(taddr + b * 32, v[b]);
           ptx::tmem_ld_wait();
-        }
-        ptx::tc_fence_before();
-        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-        if (++acc == TC_ACC_BUFS) { acc = 0; aphase ^= 1; }
-        if (!active) continue;
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
 
-        int nfin = 0;
-        int64_t fin0 = doc;
-        float* mypart = part + (tile_parity * 4 + ew) * TC_MAX_TILE_N;
-#pragma unroll
-        for (int b = 0; b < TC_MAX_TILE_N / 32; ++b) {
-          if (b * 32 >= ncols) break;
-          const int nc = min(32, ncols - b * 32);
-          const int64_t g0 = tbase + b * 32;
-          int s = 0;
+          // skip documents that ended before this tile (other groups' tiles)
+          int64_t cur_end;
           while (true) {
-            const int64_t end_rel = doc_end - g0;
-            const int e = (int)(end_rel < nc ? end_rel : nc);
-            float m = cur;
-            if (s == 0 && e == 32) {
-              float a[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) a[j] = fmaxf(v[b][j], v[b][j + 16]);
-#pragma unroll
-              for (int w = 8; w > 0; w >>= 1)
-#pragma unroll
-                for (int j = 0; j < w; ++j) a[j] = fmaxf(a[j], a[j + w]);
-              m = fmaxf(m, a[0]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j >= s && j < e) m = fmaxf(m, v[b][j]);
+            if (doc - win >= 32) {
+              win += 32;
+              ends = ends_nx;
+              ends_nx = (win + 32 + lane < c.doc1) ? __ldg(p.d_tok_off + win + 33 + lane) : INT64_MAX;
+              continue;
             }
-            cur = m;
-            if (end_rel > nc) break;  // document continues past this block
-            // document `doc` ends inside this block: finalize it
-            float x = warp_sum(lane_valid ? cur : 0.0f);
-            if (nact == 1) {
-              if (lane == 0) p.scores[doc] = x;
+            cur_end = __shfl_sync(0xffffffffu, ends, (int)(doc - win));
+            if (cur_end > tb) break;
+            prev_end = cur_end;
+            ++doc;
+          }
+          const bool head_before = prev_end < tb;
+          const int64_t head_doc = doc;
+          int nfin = 0;
+          float* mypart = part + (pb * 4 + quad) * TC_MAX_TILE_N;
+          int64_t* mydocs = part_doc + (pb * 2 + grp) * TC_MAX_TILE_N;
+          auto finalize = [&](int64_t d, float val) {
+            const float x = warp_sum(lane_valid ? val : 0.0f);
+            if (nq == 1) {
+              if (lane == 0) p.scores[d] = x;
             } else {
-              if (lane == 0) mypart[nfin] = x;
+              if (lane == 0) {
+                mypart[nfin] = x;
+                if (wig == 0) mydocs[nfin] = d;
+              }
             }
             ++nfin;
+          };
+          float cur = init, H = init;
+          bool head_open = true;
+          int end_rel = (int)(cur_end - tb < 1 << 20 ? cur_end - tb : 1 << 20);
+          auto close_seg = [&]() {
+            if (head_open) {
+              H = cur;
+              head_open = false;
+            } else {
+              finalize(doc, cur);
+            }
             cur = init;
+            prev_end = cur_end;
             ++doc;
-            if (doc - win == 32) {
-              win = doc;
-              ends = (win + lane < c.doc1) ? __ldg(p.d_tok_off + win + 1 + lane) : INT64_MAX;
+            if (doc - win >= 32) {
+              win += 32;
+              ends = ends_nx;
+              ends_nx = (win + 32 + lane < c.doc1) ? __ldg(p.d_tok_off + win + 33 + lane) : INT64_MAX;
             }
-            doc_end = __shfl_sync(0xffffffffu, ends, (int)(doc - win));
-            s = e;
-            if (s >= nc) break;
-          }
-        }
-        if (nact > 1) {
-          // combine per-quadrant partial sums in a fixed order
-          asm volatile("bar.sync 1, %0;" ::"r"(nact * 32) : "memory");
-          if (ew == 0) {
-            const float* pp = part + tile_parity * 4 * TC_MAX_TILE_N;
-            for (int j = lane; j < nfin; j += 32) {
-              float sacc = pp[j];
-              for (int w = 1; w < nact; ++w) sacc += pp[w * TC_MAX_TILE_N + j];
-              p.scores[fin0 + j] = sacc;
+            cur_end = __shfl_sync(0xffffffffu, ends, (int)(doc - win));
+            end_rel = (int)(cur_end - tb < 1 << 20 ? cur_end - tb : 1 << 20);
+          };
+#pragma unroll
+          for (int b = 0; b < TC_MAX_TILE_N / 32; ++b) {
+            if (b * 32 >= ncols) break;
+            const int g0 = b * 32;
+            const int nc = ncols - g0 < 32 ? ncols - g0 : 32;
+            if (end_rel >= g0 + nc) {
+              // no document boundary strictly inside this block
+              cur = fmaxf(cur, nc == 32 ? max32(v[b]) : masked_max(v[b], 0, nc, init));
+              if (end_rel == g0 + nc) close_seg();
+            } else {
+              int s = 0;
+              while (true) {
+                const int e = end_rel - g0 < nc ? end_rel - g0 : nc;
+                cur = masked_max(v[b], s, e, cur);
+                if (end_rel - g0 > nc) break;
+                close_seg();
+                s = e;
+                if (s >= nc) break;
+              }
             }
           }
-          tile_parity ^= 1;
+          // carry chain: merge the previous tile's open document into this head
+          float p_prev = init;
+          if (tg > 0) {
+            const uint32_t ps = (tg - 1) & 3;
+            ptx::mbar_wait(&cfull[ps], ((tg - 1) >> 2) & 1);
+            p_prev = carry[(ps * 4 + wig) * 32 + lane];
+          }
+          float p_new, head_final = 0.0f;
+          if (head_open) {
+            p_new = head_before ? fmaxf(p_prev, cur) : cur;
+          } else {
+            head_final = head_before ? fmaxf(p_prev, H) : H;
+            p_new = cur;
+          }
+          carry[((tg & 3) * 4 + wig) * 32 + lane] = p_new;
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&cfull[tg & 3]);
+          if (!head_open) finalize(head_doc, head_final);
+          if (nq > 1) {
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(nq * 32) : "memory");
+            if (wig == 0) {
+              for (int j = lane; j < nfin; j += 32) {
+                float sacc = part[(pb * 4 + grp * nq) * TC_MAX_TILE_N + j];
+                for (int w = 1; w < nq; ++w) sacc += part[(pb * 4 + grp * nq + w) * TC_MAX_TILE_N + j];
+                p.scores[mydocs[j]] = sacc;
+              }
+            }
+            pb ^= 1;
+          }
         }
       }
     }
@@ -349,19 +451,18 @@ int launch_maxsim_tc(const cbx_batch* b, float* scores, cudaStream_t stream) {
   if (!tc_supported(b)) return fail(CBX_EINVAL, "tcgen05 scorer needs f16/bf16 tokens, Lq <= 128, dim % 8 == 0");
   if (b->n_docs == 0 || b->n_queries == 0) return CBX_OK;
   const int kblocks = (b->dim + 63) / 64;
-  const int tile_n = kblocks <= 2 ? 128 : 64;
-  const int lqp = (b->max_lq + 7) / 8 * 8;
-  const uint32_t q_slot_bytes = (uint32_t)(kblocks * lqp * 128);
+  const int tile_n = kblocks <= 2 ? 128 : (kblocks <= 4 ? 64 : 32);
+  const int nq = (b->max_lq + 31) / 32;
+  const int rep = nq == 3 ? 1 : 4 / nq;
+  const int lqp = nq * 32;
+  const uint32_t q_slot_bytes = (uint32_t)(kblocks * 128 * 128);
   const uint32_t stage_bytes = (uint32_t)(kblocks * tile_n * 128);
-  const size_t bar_bytes = 512 + 2 * 4 * TC_MAX_TILE_N * sizeof(float);  // barriers + partial sums
-  const size_t budget = 227 * 1024 - 1024 /*align slack*/ - bar_bytes - 2 * q_slot_bytes;
+  const size_t bar_bytes = 512 + (4 * 4 * 32 + 2 * 4 * TC_MAX_TILE_N) * sizeof(float) +
+                           2 * 2 * TC_MAX_TILE_N * sizeof(int64_t);
+  const size_t budget = 227 * 1024 - 1024 /*align slack*/ - bar_bytes - q_slot_bytes;
   int stages = (int)std::min<size_t>(TC_MAX_STAGES, budget / stage_bytes);
   if (stages < 2) return fail(CBX_EINVAL, "tcgen05 scorer: query tile too large for shared memory");
-  // the A operand always spans 128 rows; rows past Lq read (ignored) bytes that must lie inside the allocation
-  const size_t smem = 1024 + 2 * (size_t)q_slot_bytes + (size_t)stages * stage_bytes + bar_bytes;
-  if ((size_t)q_slot_bytes + (size_t)(kblocks - 1) * lqp * 128 + 128 * 128 >
-      2 * (size_t)q_slot_bytes + (size_t)stages * stage_bytes)
-    return fail(CBX_EINTERNAL, "tcgen05 scorer: shared layout too small for the 128-row A operand");
+  const size_t smem = 1024 + (size_t)q_slot_bytes + (size_t)stages * stage_bytes + bar_bytes;
 
   CUtensorMap tmd, tmq;
   int rc = make_tmap(&tmd, b->d_tokens, b->dtype, b->n_d_tokens, b->dim, (uint32_t)tile_n);
@@ -375,26 +476,22 @@ int launch_maxsim_tc(const cbx_batch* b, float* scores, cudaStream_t stream) {
   p.d_tok_off = b->d_tok_off;
   p.q_doc_off = b->q_doc_off;
   p.scores = scores;
-  // chunk window: enough chunks for ~6 per SM, never below 4 tiles or above 32k tokens
-  int64_t total = std::max<int64_t>(b->n_d_tokens, 1);
-  int64_t T = total / ((int64_t)nsm * 6);
-  T = std::max<int64_t>(T, 4 * tile_n);
-  T = std::min<int64_t>(T, 32768);
-  T = (T + tile_n - 1) / tile_n * tile_n;
-  p.chunk_tokens = T;
-  p.chunks_per_query = std::max<int64_t>(1, (b->max_q_doc_tokens + T - 1) / T);
-  p.n_chunks = p.chunks_per_query * b->n_queries;
+  p.n_queries = b->n_queries;
+  p.n_docs = b->n_docs;
+  p.n_tokens = b->n_d_tokens;
   p.idesc = ptx::idesc_f16(b->dtype == CBX_BF16, 128, (uint32_t)tile_n);
   p.tile_n = tile_n;
   p.kblocks = kblocks;
   p.lqp = lqp;
+  p.nq = nq;
+  p.rep = rep;
   p.stages = stages;
   p.clamp_negative = b->clamp_negative;
   p.q_slot_bytes = q_slot_bytes;
   p.stage_bytes = stage_bytes;
 
   CBX_CUDA_CHECK(cudaFuncSetAttribute(maxsim_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int grid = (int)std::min<int64_t>(p.n_chunks, nsm);
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(b->n_docs, nsm));
   maxsim_tc_kernel<<<grid, TC_THREADS, smem, stream>>>(tmd, tmq, p);
   CBX_LAUNCH_CHECK("maxsim_tc_kernel launch");
   return CBX_OK;
