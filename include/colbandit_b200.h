@@ -150,24 +150,26 @@ typedef struct cbx_pcg64 {
 /* One bandit run (BanditConfig, colbandit/bandit.py:40-76). log_term is
  * RadiusConfig.log_term(N, T) evaluated on the host with math.log
  * (bounds.py:138-143). For CBX_STATIC_WARMUP the host draws the warm-up
- * cells with numpy's Generator.choice and passes them (and the generator
- * state after that draw) in warm_cells / rng. */
+ * cells with numpy's Generator.choice (bandit.py:152) and passes them, in
+ * draw order, at warm_cells[warm_off ...] together with the generator state
+ * after that draw; every other draw happens on the device. */
 typedef struct cbx_bandit_run_desc {
-  int64_t query;          /* query index in the batch (token source)          */
-  int64_t doc_begin;      /* first document (global index) of the pool        */
-  int32_t n_docs;         /* pool size N                                      */
-  int32_t k;              /* Top-K target (1 <= k <= N; k == 0 handled on host)*/
+  int64_t query;          /* token source: query index in the batch           */
+  int64_t row_begin;      /* global doc index (token source) or matrix row of row 0 */
+  int32_t n_rows;         /* pool size N                                      */
+  int32_t n_cols;         /* T (query tokens), 1..64                          */
+  int32_t k;              /* Top-K target, 1..N (k == 0 is answered on the host) */
   int32_t explore_mode;   /* CBX_EPSILON_GREEDY / CBX_STATIC_WARMUP / CBX_UNIFORM_ROW */
   int32_t n_warm;         /* static warm-up cell count                        */
+  int32_t pad0;
   int64_t warm_off;       /* offset of this run's cells in warm_cells         */
   double alpha_ef;
   double epsilon;
   double log_term;
-  int64_t bounds_off;     /* element offset of this run's (N x T) lo/hi block, -1 = uniform */
+  int64_t bounds_off;     /* element offset of this run's row-major N x T lo/hi block; -1 = uniform */
   double lo_uniform;      /* generic bounds when bounds_off < 0 (bounds.py:177-180) */
   double hi_uniform;
-  int64_t trace_off;      /* offset of this run's trace slots                 */
-  int64_t trace_cap;      /* capacity (>= N*T is always enough)               */
+  int64_t trace_off;      /* offset of this run's N*T trace slots             */
   int64_t state_off;      /* offset (in rows) of this run's per-row state     */
   cbx_pcg64 rng;
 } cbx_bandit_run_desc;
@@ -176,28 +178,28 @@ typedef struct cbx_bandit_out {
   int64_t n_reveals;
   int32_t iterations;
   int32_t terminated_by;  /* CBX_TERM_* */
-  int32_t status;         /* 0 ok; nonzero = device-detected error (see cbx_last_error) */
+  int32_t status;         /* 0 ok; 1 both boundary rows exhausted (RuntimeError in the
+                             reference, bandit.py:311-312); 2 exact-sum capacity exceeded */
   int32_t pad;
 } cbx_bandit_out;
 
-/* Cell source: either token embeddings (cells computed on demand in float64
- * from the batch — MaxSimOracle(query, docs)) or a precomputed float64
- * matrix (MaxSimOracle.from_matrix, oracle.py:146-176): cell (i, t) of run r
- * at matrix[(doc_begin + i) * ld_matrix + t]. */
-CBX_API size_t cbx_bandit_state_bytes(int64_t total_rows, int32_t max_t);
+/* Device scratch for `total_rows` rows over all runs of one call. */
+CBX_API size_t cbx_bandit_state_bytes(int64_t total_rows);
 
-CBX_API int cbx_bandit_run(const cbx_batch* b,              /* token source or NULL   */
-                   const double* matrix, int64_t ld_matrix, int32_t n_cols,
-                   const cbx_bandit_run_desc* runs, /* device array [n_runs]  */
-                   int64_t n_runs,
-                   const double* bounds_lo, const double* bounds_hi,
-                   const int32_t* warm_cells,       /* flat cell ids (i*T+t)  */
-                   void* row_state, size_t state_bytes,
-                   int32_t* topk,                   /* [n_runs * max_k]       */
-                   int32_t max_k,
-                   int32_t* trace_i, int32_t* trace_t, double* trace_v,
-                   cbx_bandit_out* out,             /* [n_runs]               */
-                   void* stream);
+/* Run n_runs independent bandits, one CTA each, entirely on the device.
+ * Cell source: token embeddings of ``b`` (cells computed on demand in float64
+ * like MaxSimOracle(query, docs), oracle.py:205-215) when b != NULL, else the
+ * float64 matrix (MaxSimOracle.from_matrix, oracle.py:146-176) with cell
+ * (i, t) of a run at matrix[(row_begin + i) * ld_matrix + t].
+ * Outputs: topk[r * max_k + j] ranked by (-proxy, row) (bandit.py:349);
+ * trace_{i,t,v}[trace_off + s] in reveal order; out[r]. */
+CBX_API int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix,
+                           const cbx_bandit_run_desc* runs, int64_t n_runs, int32_t max_rows,
+                           const double* bounds_lo, const double* bounds_hi,
+                           const int32_t* warm_cells, void* state, size_t state_bytes,
+                           int32_t* topk, int32_t max_k,
+                           int32_t* trace_i, int32_t* trace_t, double* trace_v,
+                           cbx_bandit_out* out, void* stream);
 
 #ifdef __cplusplus
 }

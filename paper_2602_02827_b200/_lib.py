@@ -55,11 +55,13 @@ class CbxPcg64(ctypes.Structure):
 class CbxBanditRunDesc(ctypes.Structure):
     _fields_ = [
         ("query", ctypes.c_int64),
-        ("doc_begin", ctypes.c_int64),
-        ("n_docs", ctypes.c_int32),
+        ("row_begin", ctypes.c_int64),
+        ("n_rows", ctypes.c_int32),
+        ("n_cols", ctypes.c_int32),
         ("k", ctypes.c_int32),
         ("explore_mode", ctypes.c_int32),
         ("n_warm", ctypes.c_int32),
+        ("pad0", ctypes.c_int32),
         ("warm_off", ctypes.c_int64),
         ("alpha_ef", ctypes.c_double),
         ("epsilon", ctypes.c_double),
@@ -68,7 +70,6 @@ class CbxBanditRunDesc(ctypes.Structure):
         ("lo_uniform", ctypes.c_double),
         ("hi_uniform", ctypes.c_double),
         ("trace_off", ctypes.c_int64),
-        ("trace_cap", ctypes.c_int64),
         ("state_off", ctypes.c_int64),
         ("rng", CbxPcg64),
     ]
@@ -100,8 +101,8 @@ SIGNATURES = {
     "cbx_topk_f64": (_I, [_P, _P, _I64, _I64, _I, _P, _P, _P, _SZ, _P]),
     "cbx_rerank_topk": (_I, [_P, _I, _I, _P, _P, _P, _P, _SZ, _P]),
     "cbx_maxsim_cells_f64": (_I, [_P, _P, _I64, _P, _P]),
-    "cbx_bandit_state_bytes": (_SZ, [_I64, _I32]),
-    "cbx_bandit_run": (_I, [_P, _P, _I64, _I32, _P, _I64, _P, _P, _P, _P, _SZ, _P, _I32, _P, _P, _P, _P, _P]),
+    "cbx_bandit_state_bytes": (_SZ, [_I64]),
+    "cbx_bandit_run": (_I, [_P, _P, _I64, _P, _I64, _I32, _P, _P, _P, _P, _SZ, _P, _I32, _P, _P, _P, _P, _P]),
 }
 
 _lib = None

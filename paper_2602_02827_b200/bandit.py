@@ -1,0 +1,248 @@
+"""Drop-in Col-Bandit ``run`` executing the whole adaptive loop in one device kernel.
+
+``BanditConfig`` / ``RunResult`` / ``run(oracle, bounds, cfg)`` keep the
+reference's fields, defaults, validation, exception types and messages
+(colbandit/bandit.py:40-350). The loop itself — warm-up, boundary selection,
+epsilon-greedy column choice with numpy's PCG64 stream, float64 reveal,
+exact-sum interval update, Top-K maintenance — runs in ``cbx_bandit_run``
+(csrc/bandit.cu) without host round trips; the host only seeds the
+generator (numpy SeedSequence, as the reference does at bandit.py:193),
+evaluates ``log_term`` with ``math.log`` and, for ``static-warmup`` only,
+draws the warm-up sample with numpy's ``Generator.choice`` (bandit.py:152).
+
+``run_batch`` launches many independent runs (queries x parameters) at once:
+one CTA per run.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from .bounds import CellBounds, RadiusConfig
+
+__all__ = ["BanditConfig", "RunResult", "EXPLORE_MODES", "run", "run_batch", "ceil_cells", "select_ambiguous",
+           "BanditJob"]
+
+EXPLORE_MODES = ("epsilon-greedy", "static-warmup", "uniform-row")
+_MODE_CODE = {"epsilon-greedy": _lib.CBX_EPSILON_GREEDY, "static-warmup": _lib.CBX_STATIC_WARMUP,
+              "uniform-row": _lib.CBX_UNIFORM_ROW}
+MAX_COLS = 64
+
+
+@dataclass(frozen=True)
+class BanditConfig:
+    """bandit.py:40-76."""
+
+    k: int
+    delta: float = 0.01
+    alpha_ef: float = 1.0
+    epsilon: float = 0.1
+    explore_mode: str = "epsilon-greedy"
+    gamma_init: float = 0.0
+    seed: int | tuple[int, ...] | None = 0
+    c: float = 1.0
+    union_mode: str = "per-document"
+
+    def __post_init__(self) -> None:
+        if self.k < 0:
+            raise ValueError(f"k must be non-negative, got {self.k}")
+        if not 0.0 <= self.epsilon <= 1.0:
+            raise ValueError(f"epsilon must be in [0, 1], got {self.epsilon}")
+        if self.explore_mode not in EXPLORE_MODES:
+            raise ValueError(f"explore_mode must be one of {EXPLORE_MODES}, got {self.explore_mode!r}")
+        if not 0.0 <= self.gamma_init <= 1.0:
+            raise ValueError(f"gamma_init must be in [0, 1], got {self.gamma_init}")
+        self.radius_config
+
+    @property
+    def radius_config(self) -> RadiusConfig:
+        return RadiusConfig(self.alpha_ef, self.delta, self.c, self.union_mode)
+
+
+@dataclass(frozen=True)
+class RunResult:
+    """bandit.py:79-95."""
+
+    topk: list[int]
+    coverage: float
+    reveals: list[tuple[int, int, float]]
+    iterations: int
+    terminated_by: str
+
+
+def ceil_cells(fraction: float, total: int) -> int:
+    """bandit.py:98-108 (snaps near-integer products before the ceiling)."""
+    x = fraction * total
+    nearest = round(x)
+    if abs(x - nearest) < 1e-9 * max(1.0, total):
+        return int(nearest)
+    return math.ceil(x)
+
+
+def select_ambiguous(i_plus: int, i_minus: int, width_plus: float, width_minus: float) -> int:
+    return i_plus if width_plus >= width_minus else i_minus
+
+
+@dataclass
+class BanditJob:
+    """One run of a batched launch: a query (or matrix block) + bounds + config."""
+
+    cfg: BanditConfig
+    n_rows: int
+    n_cols: int
+    query: int = 0          # token source: query index in the batch
+    row_begin: int = 0      # global doc index (token source) / matrix row of row 0
+    bounds: CellBounds | tuple[float, float] = (-1.0, 1.0)
+
+
+def _rng_state(seed, explore_mode, gamma_init, total_cells):
+    """numpy seeding (+ the static warm-up draw) on the host; returns (pcg64 struct, warm cells)."""
+    g = np.random.default_rng(seed)
+    warm = np.zeros(0, dtype=np.int32)
+    if explore_mode == "static-warmup":
+        m = ceil_cells(gamma_init, total_cells)
+        if m:
+            warm = np.asarray(g.choice(total_cells, size=m, replace=False), dtype=np.int32)
+    st = g.bit_generator.state
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    p = _lib.CbxPcg64()
+    p.state_hi, p.state_lo = s >> 64, s & ((1 << 64) - 1)
+    p.inc_hi, p.inc_lo = inc >> 64, inc & ((1 << 64) - 1)
+    p.has_uint32 = int(st["has_uint32"])
+    p.uinteger = int(st["uinteger"])
+    return p, warm
+
+
+def run_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, return_traces: bool = True, sync: bool = True):
+    """Launch every job in one kernel; returns a list of RunResult (or raw device outputs if sync=False)."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    if batch is None and matrix is None:
+        raise ValueError("need a TokenBatch or a device matrix as the cell source")
+    n = len(jobs)
+    descs = (_lib.CbxBanditRunDesc * max(n, 1))()
+    lo_parts, hi_parts, warm_parts = [], [], []
+    b_off = w_off = tr_off = st_off = 0
+    max_rows = max_k = 1
+    results: list = [None] * n
+    live = []
+    for r, job in enumerate(jobs):
+        cfg = job.cfg
+        N, T = int(job.n_rows), int(job.n_cols)
+        if T > MAX_COLS:
+            raise ValueError(f"the device bandit supports at most {MAX_COLS} query tokens, got {T}")
+        if cfg.k > N:
+            raise ValueError(f"k={cfg.k} exceeds the number of documents ({N})")
+        if cfg.k == 0:
+            results[r] = RunResult([], 0.0, [], 0, "separation")
+            continue
+        d = descs[len(live)]
+        live.append(r)
+        d.query, d.row_begin, d.n_rows, d.n_cols, d.k = job.query, job.row_begin, N, T, cfg.k
+        d.explore_mode = _MODE_CODE[cfg.explore_mode]
+        d.alpha_ef, d.epsilon = cfg.alpha_ef, cfg.epsilon
+        d.log_term = cfg.radius_config.log_term(N, T)
+        bnd = job.bounds
+        uni = bnd if isinstance(bnd, tuple) else bnd.uniform_values()
+        if uni:
+            d.bounds_off = -1
+            d.lo_uniform, d.hi_uniform = uni
+        else:
+            d.bounds_off = b_off
+            lo_parts.append(np.ascontiguousarray(bnd.lo, dtype=np.float64).ravel())
+            hi_parts.append(np.ascontiguousarray(bnd.hi, dtype=np.float64).ravel())
+            b_off += N * T
+        d.rng, warm = _rng_state(cfg.seed, cfg.explore_mode, cfg.gamma_init, N * T)
+        d.n_warm, d.warm_off = len(warm), w_off
+        warm_parts.append(warm)
+        w_off += len(warm)
+        d.trace_off, d.state_off = tr_off, st_off
+        tr_off += N * T
+        st_off += N
+        max_rows, max_k = max(max_rows, N), max(max_k, cfg.k)
+    nl = len(live)
+    if nl == 0:
+        return results
+    dev = torch.device("cuda", torch.cuda.current_device())
+    desc_t = torch.frombuffer(bytearray(bytes(descs)[: nl * ctypes.sizeof(_lib.CbxBanditRunDesc)]),
+                              dtype=torch.uint8).to(dev)
+    lo_t = torch.from_numpy(np.concatenate(lo_parts)).to(dev) if lo_parts else None
+    hi_t = torch.from_numpy(np.concatenate(hi_parts)).to(dev) if hi_parts else None
+    warm_t = torch.from_numpy(np.concatenate(warm_parts)).to(dev) if w_off else None
+    state_bytes = lib.cbx_bandit_state_bytes(st_off)
+    state = torch.empty(state_bytes, dtype=torch.uint8, device=dev)
+    topk_t = torch.empty((nl, max_k), dtype=torch.int32, device=dev)
+    tr_i = torch.empty(max(tr_off, 1), dtype=torch.int32, device=dev)
+    tr_t = torch.empty(max(tr_off, 1), dtype=torch.int32, device=dev)
+    tr_v = torch.empty(max(tr_off, 1), dtype=torch.float64, device=dev)
+    out_t = torch.empty(nl * ctypes.sizeof(_lib.CbxBanditOut), dtype=torch.uint8, device=dev)
+    bstruct = batch.struct() if batch is not None else None
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    ld = matrix.shape[1] if matrix is not None else 0
+    _lib.check(lib.cbx_bandit_run(
+        ctypes.byref(bstruct) if bstruct is not None else None,
+        matrix.data_ptr() if matrix is not None else None, ld,
+        desc_t.data_ptr(), nl, max_rows,
+        lo_t.data_ptr() if lo_t is not None else None, hi_t.data_ptr() if hi_t is not None else None,
+        warm_t.data_ptr() if warm_t is not None else None, state.data_ptr(), state_bytes,
+        topk_t.data_ptr(), max_k, tr_i.data_ptr(), tr_t.data_ptr(), tr_v.data_ptr(), out_t.data_ptr(), stream),
+        "bandit_run")
+    raw = dict(descs=descs, live=live, topk=topk_t, tr_i=tr_i, tr_t=tr_t, tr_v=tr_v, out=out_t,
+               keep=(desc_t, lo_t, hi_t, warm_t, state))
+    if not sync:
+        return raw
+    return collect(raw, jobs, results, return_traces)
+
+
+def collect(raw, jobs, results=None, return_traces: bool = True):
+    """Fetch a launch's device outputs and build RunResults (raises on device-side errors)."""
+    if results is None:
+        results = [None] * len(jobs)
+    live = raw["live"]
+    out = np.frombuffer(raw["out"].cpu().numpy().tobytes(), dtype=np.dtype(
+        [("n_reveals", "<i8"), ("iterations", "<i4"), ("terminated_by", "<i4"), ("status", "<i4"), ("pad", "<i4")]))
+    topk = raw["topk"].cpu().numpy()
+    if return_traces:
+        tr_i, tr_t, tr_v = (raw[k].cpu().numpy() for k in ("tr_i", "tr_t", "tr_v"))
+    for slot, r in enumerate(live):
+        job, o, d = jobs[r], out[slot], raw["descs"][slot]
+        if o["status"] == 1:
+            raise RuntimeError("internal error: both boundary rows exhausted while unseparated")
+        if o["status"] != 0:
+            raise RuntimeError(f"bandit kernel status {int(o['status'])} (exact-sum capacity exceeded)")
+        nrev = int(o["n_reveals"])
+        reveals = []
+        if return_traces:
+            a = d.trace_off
+            reveals = list(zip(tr_i[a:a + nrev].tolist(), tr_t[a:a + nrev].tolist(), tr_v[a:a + nrev].tolist()))
+        term = "separation" if o["terminated_by"] == _lib.CBX_TERM_SEPARATION else "exhaustion"
+        results[r] = RunResult([int(x) for x in topk[slot, : job.cfg.k]], nrev / (job.n_rows * job.n_cols),
+                               reveals, int(o["iterations"]), term)
+    return results
+
+
+def run(oracle, bounds: CellBounds, cfg: BanditConfig) -> RunResult:
+    """Identify the Top-K rows revealing as few cells as the intervals allow (bandit.py:169-350)."""
+    n_rows, n_cols = oracle.n_docs, oracle.n_query_tokens
+    if (bounds.n_rows, bounds.n_cols) != (n_rows, n_cols):
+        raise ValueError(
+            f"bounds shape ({bounds.n_rows}, {bounds.n_cols}) does not match matrix shape ({n_rows}, {n_cols})")
+    if cfg.k > n_rows:
+        raise ValueError(f"k={cfg.k} exceeds the number of documents ({n_rows})")
+    if cfg.k == 0:
+        return RunResult([], 0.0, [], 0, "separation")
+    if not hasattr(oracle, "_batch"):
+        raise TypeError("run() needs a paper_2602_02827_b200 MaxSimOracle (device-resident cells)")
+    job = BanditJob(cfg, n_rows, n_cols, 0, 0, bounds)
+    if oracle._batch is not None:
+        res = run_batch([job], batch=oracle._batch)[0]
+    else:
+        res = run_batch([job], matrix=oracle._dev_matrix)[0]
+    oracle._reveal_count += len(res.reveals)
+    return res

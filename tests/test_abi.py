@@ -38,6 +38,7 @@ def test_struct_layouts_match_the_header():
     assert ctypes.sizeof(_lib.CbxBatch) == 5 * 8 + 4 * 8 + 4 * 4 + 2 * 8
     assert ctypes.sizeof(_lib.CbxPcg64) == 4 * 8 + 2 * 4
     assert ctypes.sizeof(_lib.CbxBanditOut) == 8 + 4 * 4
+    assert ctypes.sizeof(_lib.CbxBanditRunDesc) == 152  # static_assert in csrc/bandit.cu
 
 
 def test_library_is_sm100a_only():

@@ -1,0 +1,199 @@
+"""P2 parity on the B200: the device Col-Bandit loop against the reference.
+
+The bar is trace-for-trace equality with the unmodified reference (golden
+vectors from tests/golden/make_golden.py) — same revealed cells in the same
+order with bit-equal float64 values, same Top-K (ranked), iterations, stop
+reason and coverage. BASELINE.json only requires the same Top-K set and a
+coverage within 2%; exact traces are the stronger check.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from helpers import case_doc_list, storage_dtype
+from oracle import bandit_ref, maxsim_ref
+from paper_2602_02827_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _seed(s):
+    return tuple(s) if isinstance(s, list) else s
+
+
+def _cases():
+    with open(os.path.join(GOLDEN, "p2_small.json")) as f:
+        return json.load(f)
+
+
+def _assert_same(res, exp, value_atol=0.0):
+    got = [(int(i), int(t)) for i, t, _ in res.reveals]
+    assert got == [(i, t) for i, t, _ in exp["reveals"]]
+    np.testing.assert_allclose([v for *_, v in res.reveals], [v for *_, v in exp["reveals"]], rtol=0,
+                               atol=value_atol)
+    assert res.topk == exp["topk"]
+    assert res.iterations == exp["iterations"]
+    assert res.terminated_by == exp["terminated_by"]
+    assert res.coverage == exp["coverage"]
+
+
+def test_matrix_backed_runs_match_reference_trace_for_trace():
+    from paper_2602_02827_b200 import BanditConfig, CellBounds, MaxSimOracle, run
+
+    n = 0
+    for case in _cases():
+        if case["source"] != "matrix":
+            continue
+        cfg = dict(case["cfg"])
+        cfg["seed"] = _seed(cfg["seed"])
+        oracle = MaxSimOracle.from_matrix(np.array(case["cells"]), value_range=(-0.7, 1.5))
+        res = run(oracle, CellBounds(np.array(case["lo"]), np.array(case["hi"])), BanditConfig(**cfg))
+        _assert_same(res, case["result"])
+        assert oracle.reveal_count == len(res.reveals)
+        n += 1
+    assert n == 36
+
+
+def test_token_backed_runs_match_reference_trace_for_trace():
+    from paper_2602_02827_b200 import (BanditConfig, CellBounds, DocTokens, MaxSimOracle, QueryTokens, Similarity,
+                                       full_rerank, run)
+
+    for case in _cases():
+        if case["source"] != "tokens":
+            continue
+        dt, d = case["dtype"], case["dim"]
+        store = {"f32": np.float32, "f16": np.float16, "bf16": np.uint16}[dt]
+        q = np.frombuffer(bytes.fromhex(case["query_hex"]), dtype=store).reshape(-1, d)
+        toks = np.frombuffer(bytes.fromhex(case["tokens_hex"]), dtype=store).reshape(-1, d)
+        off = case["offsets"]
+        if dt == "bf16":
+            from paper_2602_02827_b200.batch import to_torch_tokens
+
+            q = to_torch_tokens(q, "bf16")
+            toks = to_torch_tokens(toks, "bf16")
+        docs = [DocTokens(f"d{i}", toks[off[i]:off[i + 1]]) for i in range(len(off) - 1)]
+        sim = Similarity("dot", -1.0, 1.0, case["clamp"])
+        oracle = MaxSimOracle(QueryTokens(q), docs, sim)
+        cfg = dict(case["cfg"])
+        cfg["seed"] = _seed(cfg["seed"])
+        lo, hi = oracle.value_range
+        res = run(oracle, CellBounds.uniform(oracle.n_docs, oracle.n_query_tokens, lo, hi), BanditConfig(**cfg))
+        _assert_same(res, case["result"], value_atol=1e-15 if dt == "f32" else 0.0)
+        full = full_rerank(MaxSimOracle(QueryTokens(q), docs, sim), cfg["k"])
+        assert full.topk == case["full_rerank"]["topk"]
+        assert len(full.reveals) == case["full_rerank"]["n_reveals"]
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5"])
+def test_config_query_bandit_matches_reference(name):
+    """One full-shape query of each BASELINE config; cfg5 sweeps all five alphas."""
+    from paper_2602_02827_b200 import BanditConfig, BanditJob, run_batch
+    from helpers import batch_of_cases
+
+    path = os.path.join(GOLDEN, f"{name}_q0.npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture missing")
+    z = np.load(path)
+    cfg = W.CONFIGS[name]
+    case = W.gen_query(name, 0)
+    b = batch_of_cases([case])
+    lq = case.query.shape[0]
+    jobs = [BanditJob(BanditConfig(k=cfg.k, alpha_ef=a, seed=(0, 0)), case.n_docs, lq, 0, 0, (-1.0, 1.0))
+            for a in cfg.alphas]
+    results = run_batch(jobs, batch=b)
+    for ai, res in enumerate(results):
+        exp_it = z[f"a{ai}_trace_it"]
+        got_it = np.array([(i, t) for i, t, _ in res.reveals], dtype=np.int32).reshape(-1, 2)
+        assert got_it.shape == exp_it.shape, (name, ai, got_it.shape, exp_it.shape)
+        np.testing.assert_array_equal(got_it, exp_it)
+        vals = np.array([v for *_, v in res.reveals])
+        if cfg.dtype == "f32":
+            np.testing.assert_allclose(vals, z[f"a{ai}_trace_v"], rtol=0, atol=1e-15)
+        else:
+            np.testing.assert_array_equal(vals, z[f"a{ai}_trace_v"])
+        assert res.topk == z[f"a{ai}_topk"].tolist()
+        cov, iters, sep = z[f"a{ai}_stats"]
+        assert res.coverage == cov and res.iterations == int(iters)
+        assert res.terminated_by == ("separation" if sep else "exhaustion")
+
+
+def test_batched_runs_match_the_cpu_oracle():
+    """Many queries x explore modes in one launch, checked against oracle/bandit_ref."""
+    from paper_2602_02827_b200 import BanditConfig, BanditJob, run_batch
+    from helpers import batch_of_cases
+
+    cases = [W.gen_query("cfg2", q, n_docs=120) for q in range(6)]
+    b = batch_of_cases(cases)
+    jobs, refs = [], []
+    start = 0
+    modes = ["epsilon-greedy", "uniform-row", "static-warmup"]
+    for qi, c in enumerate(cases):
+        cells = maxsim_ref.cell_matrix(c.query64(), c.docs64())
+        for mi, mode in enumerate(modes):
+            kw = dict(k=5 + qi, alpha_ef=[1.0, 0.3, 0.05][mi], explore_mode=mode, seed=(7, qi),
+                      gamma_init=0.1 if mode == "static-warmup" else 0.0)
+            jobs.append(BanditJob(BanditConfig(**kw), c.n_docs, 32, qi, start, (-1.0, 1.0)))
+            refs.append(bandit_ref.run(cells, -1.0, 1.0, **kw))
+        start += c.n_docs
+    got = run_batch(jobs, batch=b)
+    for g, r in zip(got, refs):
+        assert g.reveals == r.reveals
+        assert g.topk == r.topk and g.iterations == r.iterations and g.coverage == r.coverage
+
+
+def test_edge_cases():
+    from paper_2602_02827_b200 import BanditConfig, CellBounds, MaxSimOracle, RunResult, run
+
+    oracle = MaxSimOracle.from_matrix([[0.6, 0.4], [0.2, 0.1]], value_range=(0.0, 1.0))
+    bounds = CellBounds.uniform(2, 2, 0.0, 1.0)
+    assert run(oracle, bounds, BanditConfig(k=0)) == RunResult([], 0.0, [], 0, "separation")
+    everyone = run(oracle, bounds, BanditConfig(k=2))
+    assert sorted(everyone.topk) == [0, 1] and everyone.reveals == [] and everyone.iterations == 1
+    with pytest.raises(ValueError, match="exceeds the number of documents"):
+        run(oracle, bounds, BanditConfig(k=3))
+    with pytest.raises(ValueError, match="does not match"):
+        run(oracle, CellBounds.uniform(3, 2, 0.0, 1.0), BanditConfig(k=1))
+    # hard bounds already separate: zero reveals, one iteration
+    o2 = MaxSimOracle.from_matrix([[1.2, 1.3], [0.5, 0.5]], value_range=(0.0, 1.5))
+    b2 = CellBounds(np.array([[1.0, 1.0], [0.0, 0.0]]), np.array([[1.5, 1.5], [0.75, 0.75]]))
+    r2 = run(o2, b2, BanditConfig(k=1))
+    assert r2.topk == [0] and r2.reveals == [] and r2.iterations == 1 and r2.terminated_by == "separation"
+
+
+def test_random_matrix_cases_against_oracle():
+    """Reference-style random parity cases (tests/test_bandit.py:257-301 generator) vs the CPU oracle."""
+    from paper_2602_02827_b200 import BanditConfig, CellBounds, MaxSimOracle, run
+
+    rng = np.random.default_rng(99)
+    for mode in ("epsilon-greedy", "static-warmup", "uniform-row"):
+        for _ in range(15):
+            n, t = int(rng.integers(3, 60)), int(rng.integers(1, 65))
+            matrix = rng.uniform(-0.2, 1.0, size=(n, t))
+            if rng.random() < 0.5:
+                lo, hi = np.full((n, t), -0.2), np.full((n, t), 1.0)
+            else:
+                lo = matrix - rng.uniform(0.0, 0.4, size=(n, t))
+                hi = matrix + rng.uniform(0.0, 0.4, size=(n, t))
+            kw = dict(k=int(rng.integers(1, n + 1)), delta=float(rng.choice([0.3, 0.05, 0.001])),
+                      alpha_ef=float(rng.choice([1.0, 0.4, 0.05])), epsilon=float(rng.choice([0.0, 0.1, 0.5, 1.0])),
+                      explore_mode=mode, gamma_init=float(rng.choice([0.0, 0.1, 0.4])) if mode == "static-warmup" else 0.0,
+                      seed=int(rng.integers(0, 2**31)), c=float(rng.choice([1.0, 2.0])),
+                      union_mode=str(rng.choice(["per-document", "per-document-and-size"])))
+            got = run(MaxSimOracle.from_matrix(matrix, value_range=(-0.7, 1.5)), CellBounds(lo, hi), BanditConfig(**kw))
+            ref = bandit_ref.run(matrix, lo, hi, **{k: v for k, v in kw.items() if k != "k"}, k=kw["k"])
+            assert got.reveals == ref.reveals
+            assert got.topk == ref.topk and got.iterations == ref.iterations
+            assert got.terminated_by == ref.terminated_by
