@@ -201,6 +201,11 @@ CBX_API int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_
                            int32_t* trace_i, int32_t* trace_t, double* trace_v,
                            cbx_bandit_out* out, void* stream);
 
+/* Profiling hook: when set (device pointer to n_runs * 8 uint64), every
+ * following cbx_bandit_run writes per-run SM-cycle counters of its phases
+ * [scan, decide, reveal, update, warm-up, total]; NULL disables. */
+CBX_API void cbx_bandit_set_profile(void* counters);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,7 +4,10 @@
 // reveal (oracle.py:243-329), the interval arithmetic (bounds.py:97-263) and
 // numpy's Generator(PCG64) draws. Trace parity with the reference needs:
 //   * float64 cells from exact products (fp16/bf16 sums are exact in fp64),
-//   * CPython math.fsum semantics for every exactly rounded sum (Expansion),
+//   * CPython math.fsum semantics for every exactly rounded sum: an exact
+//     int64 fixed-point accumulator (scale 2^48) while every revealed value is
+//     a multiple of 2^-48 (always true for fp16 token inputs), otherwise a
+//     Shewchuk expansion (Expansion) — both round correctly, like fsum,
 //   * no FMA contraction and Python's left-to-right evaluation order in the
 //     bound arithmetic (this translation unit is built with -fmad=false and
 //     spells every operation with an explicit _rn intrinsic),
@@ -12,28 +15,64 @@
 //     with no draw for n == 1, random() = (next64 >> 11) * 2^-53,
 //   * the loop's control flow: lazy warm-up counted as an iteration, the
 //     exhausted-boundary-row switch, ties to the lower row index.
-// Ranking state (proxy / lcb / ucb / Top-K membership) lives in shared memory
-// when the pool fits, otherwise in global memory; per-row statistics (count,
-// Welford mean / m2, unrevealed-column mask, exact-sum expansions) live in
-// global memory and are touched only for the revealed row.
+//
+// Per-iteration latency chain (one CTA, 256 threads): scan the pool for the
+// four boundary selections (warp redux) -> warp 0 picks i*, t* (PCG64) ->
+// G-lane groups dot the document's tokens with q_t* (all loads in flight,
+// float64 accumulate) -> thread 0 updates the row (Welford, exact sum,
+// interval from precomputed sqrt tables) and the Top-K membership.
+// Ranking and per-row state live in shared memory when the pool fits,
+// otherwise in global memory.
 #include "common.cuh"
 
 namespace cbx {
 
 constexpr int BD_THREADS = 256;
 constexpr int BD_WARPS = BD_THREADS / 32;
-constexpr int BD_CAP = 8;              // exact-sum expansion capacity per row
-constexpr int BD_SMEM_ROWS = 4096;     // pools up to this size keep ranking state in smem
-
-struct RowState {
-  double mean, m2;
-  uint64_t unrev;  // bit t set = column t not yet revealed
-  int32_t n, pad;
-  Expansion<BD_CAP> obs, lo_un, hi_un;
-};
+constexpr int BD_CAP = 8;              // exact-sum expansion capacity (CPython fsum partials)
+constexpr int BD_SMEM_ROWS = 2560;     // pools up to this size keep all per-row state in shared memory
+constexpr int BD_MAX_T = 64;
+constexpr double BD_FX_SCALE = 281474976710656.0;        // 2^48
+constexpr double BD_FX_INV = 1.0 / 281474976710656.0;    // 2^-48
+constexpr double BD_FX_LIMIT = 36028797018963968.0;      // 2^55: 64 terms stay below 2^61
 
 static_assert(sizeof(cbx_bandit_run_desc) == 152, "cbx_bandit_run_desc layout");
 static_assert(sizeof(cbx_bandit_out) == 24, "cbx_bandit_out layout");
+
+// Persistent exact-sum expansion in global memory.
+struct ExpStore {
+  double p[BD_CAP];
+  int32_t n, pad;
+};
+
+// Per-row state, structure of arrays: shared memory for small pools, global otherwise.
+struct RowsView {
+  double* proxy;
+  double* lcb;
+  double* ucb;
+  double* mean;        // Welford running mean (oracle.py:307-310)
+  double* m2;          // Welford sum of squared deviations
+  long long* fx;       // exact sum of revealed values x 2^48 while every value is on that grid
+  uint64_t* unrev;     // bit t set = column t not yet revealed
+  uint64_t* wkey;      // warm-up scratch: ordered key of the row's warm-up cell
+  int32_t* cnt;        // revealed cells per row
+  uint8_t* exp_mode;   // 1: the row's exact sum lives in the global expansion store
+  uint8_t* member;     // Top-K membership
+  __device__ void carve(uint8_t* base, int N) {
+    proxy = reinterpret_cast<double*>(base);
+    lcb = proxy + N;
+    ucb = lcb + N;
+    mean = ucb + N;
+    m2 = mean + N;
+    fx = reinterpret_cast<long long*>(m2 + N);
+    unrev = reinterpret_cast<uint64_t*>(fx + N);
+    wkey = unrev + N;
+    cnt = reinterpret_cast<int32_t*>(wkey + N);
+    exp_mode = reinterpret_cast<uint8_t*>(cnt + N);
+    member = exp_mode + N;
+  }
+};
+constexpr size_t ROW_BYTES = 8 * 8 + 4 + 1 + 1;
 
 struct BanditParams {
   // token source (nullptr q_tokens -> matrix source)
@@ -49,9 +88,10 @@ struct BanditParams {
   const double* bounds_lo;
   const double* bounds_hi;
   const int32_t* warm_cells;
-  RowState* rows;
-  double* g_rank;      // [total_rows * 3] proxy, lcb, ucb when not in smem
-  uint8_t* g_member;   // [total_rows]
+  ExpStore* g_obs;     // [rows] exact sums of rows that left the 2^-48 grid
+  ExpStore* g_lo;      // [rows] sum of lo over unrevealed columns (per-cell bounds only)
+  ExpStore* g_hi;      // [rows]
+  uint8_t* g_rows;     // [rows * ROW_BYTES] per-row state when it does not fit in smem
   int use_smem;
   int32_t* topk;
   int32_t max_k;
@@ -59,6 +99,7 @@ struct BanditParams {
   int32_t* trace_t;
   double* trace_v;
   cbx_bandit_out* out;
+  unsigned long long* prof;  // optional per-run phase cycle counters (cbx_bandit_set_profile)
 };
 
 // ----------------------------------------------------------------- Python semantics
@@ -110,56 +151,52 @@ struct Pcg64 {
   }
 };
 
-// ----------------------------------------------------------------- keyed reductions
-struct KeyIdx {
-  double k;
-  int32_t i;  // -1 = empty
+// ----------------------------------------------------------------- keyed selections
+// order-preserving double <-> uint64
+__device__ __forceinline__ uint64_t ord_key(double x) {
+  uint64_t u = (uint64_t)__double_as_longlong(x);
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(uint64_t k) {
+  uint64_t u = (k & 0x8000000000000000ull) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+// A selection candidate: maximise `key`, break ties by minimising `tie`
+// (key 0 = empty). The four selections of the loop map onto it as
+//   i+      : key = ~ord(lcb),  tie = i          argmin (lcb, i) over the Top-K
+//   i-      : key = ord(ucb),   tie = i          argmax ucb over the rest, lowest i
+//   best    : key = ord(proxy), tie = i          first non-member in (-proxy, i)
+//   worst   : key = ~ord(proxy), tie = ~i        last member in (-proxy, i)
+struct Cand {
+  uint64_t key;
+  uint32_t tie;
 };
-
-// "a is preferred over b" for the four selections of the loop
-enum { SEL_MIN_LCB = 0, SEL_MAX_UCB = 1, SEL_MAX_PROXY = 2, SEL_WORST_PROXY = 3 };
-
-__device__ __forceinline__ bool prefer(int sel, const KeyIdx& a, const KeyIdx& b) {
-  if (b.i < 0) return a.i >= 0;
-  if (a.i < 0) return false;
-  switch (sel) {
-    case SEL_MIN_LCB: return a.k < b.k || (a.k == b.k && a.i < b.i);      // argmin (lcb, i)
-    case SEL_MAX_UCB: return a.k > b.k || (a.k == b.k && a.i < b.i);      // argmax ucb, lowest i
-    case SEL_MAX_PROXY: return a.k > b.k || (a.k == b.k && a.i < b.i);    // first in (-proxy, i)
-    default: return a.k < b.k || (a.k == b.k && a.i > b.i);               // last in (-proxy, i)
+__device__ __forceinline__ void cand_take(Cand& a, uint64_t key, uint32_t tie) {
+  if (key > a.key || (key == a.key && tie < a.tie)) {
+    a.key = key;
+    a.tie = tie;
   }
 }
-
-__device__ __forceinline__ KeyIdx shfl_ki(const KeyIdx& v, int off) {
-  KeyIdx r;
-  r.k = __shfl_xor_sync(0xffffffffu, v.k, off);
-  r.i = __shfl_xor_sync(0xffffffffu, v.i, off);
-  return r;
+// warp-wide winner: two 32-bit max reductions + one min
+__device__ __forceinline__ Cand warp_best(Cand c) {
+  const uint32_t hi = (uint32_t)(c.key >> 32);
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t lo = hi == mh ? (uint32_t)c.key : 0u;
+  const uint32_t ml = __reduce_max_sync(0xffffffffu, lo);
+  const uint64_t best = ((uint64_t)mh << 32) | ml;
+  const uint32_t t = __reduce_min_sync(0xffffffffu, c.key == best ? c.tie : 0xFFFFFFFFu);
+  return Cand{best, t};
 }
-
-__device__ __forceinline__ void warp_select(int sel, KeyIdx& v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    KeyIdx w = shfl_ki(v, o);
-    if (prefer(sel, w, v)) v = w;
-  }
-}
+constexpr uint32_t TIE_EMPTY = 0xFFFFFFFFu;
 
 // ----------------------------------------------------------------- row arithmetic
-// refresh(i) of bandit.py:220-247 / compute_decision_state (bounds.py:244-256)
-__device__ void row_interval(const RowState& s, int T, bool uniform, double lo_u, double hi_u, double alpha,
-                             double log_term, double& proxy, double& lcb, double& ucb) {
-  const int n = s.n;
-  const double obs = s.obs.round();
-  double lo_sum, hi_sum;
-  if (uniform) {
-    // fsum of (T - n) copies of a constant == the correctly rounded product
-    lo_sum = (T - n) ? __dmul_rn((double)(T - n), lo_u) : 0.0;
-    hi_sum = (T - n) ? __dmul_rn((double)(T - n), hi_u) : 0.0;
-  } else {
-    lo_sum = s.lo_un.round();
-    hi_sum = s.hi_un.round();
-  }
+// refresh(i) of bandit.py:220-247 / compute_decision_state (bounds.py:244-256);
+// sq_log[n] = sqrt(2 log_term / n) and sq_rho[n] = sqrt(rho_n) come from tables
+// built with the same operations (bounds.py:105-109, 158).
+__device__ __forceinline__ void row_interval(int n, double m2, double obs, double lo_sum, double hi_sum, int T,
+                                             double alpha, const double* sq_log, const double* sq_rho,
+                                             double& proxy, double& lcb, double& ucb) {
   const double h_lo = __dadd_rn(obs, lo_sum);
   const double h_hi = __dadd_rn(obs, hi_sum);
   if (n == 0) {
@@ -175,88 +212,144 @@ __device__ void row_interval(const RowState& s, int T, bool uniform, double lo_u
     ucb = h_hi;
     return;
   }
-  const double sigma = __dsqrt_rn(__ddiv_rn(pymax(s.m2, 0.0), (double)(n - 1)));
-  double rho;
-  if (2 * n <= T) rho = __dsub_rn(1.0, __ddiv_rn((double)(n - 1), (double)T));
-  else rho = __dmul_rn(__dsub_rn(1.0, __ddiv_rn((double)n, (double)T)), __dadd_rn(1.0, __ddiv_rn(1.0, (double)n)));
+  const double sigma = __dsqrt_rn(__ddiv_rn(pymax(m2, 0.0), (double)(n - 1)));
   double r = __dmul_rn(alpha, (double)T);
   r = __dmul_rn(r, sigma);
-  r = __dmul_rn(r, __dsqrt_rn(__ddiv_rn(__dmul_rn(2.0, log_term), (double)n)));
-  r = __dmul_rn(r, __dsqrt_rn(rho));
+  r = __dmul_rn(r, sq_log[n]);
+  r = __dmul_rn(r, sq_rho[n]);
   lcb = pymin(pymax(h_lo, __dsub_rn(est, r)), h_hi);
   ucb = pymax(pymin(h_hi, __dadd_rn(est, r)), h_lo);
 }
 
-// ledger._record (oracle.py:305-314): mask, count, Welford, exact sums
-__device__ __forceinline__ bool record(RowState& s, int t, double v, bool uniform, const double* lo_row,
-                                       const double* hi_row) {
-  s.unrev &= ~(1ull << t);
-  s.n += 1;
-  const double d = __dsub_rn(v, s.mean);
-  s.mean = __dadd_rn(s.mean, __ddiv_rn(d, (double)s.n));
-  s.m2 = __dadd_rn(s.m2, __dmul_rn(d, __dsub_rn(v, s.mean)));
-  bool ok = s.obs.add(v);
-  if (!uniform) {
-    ok &= s.lo_un.add(-lo_row[t]);
-    ok &= s.hi_un.add(-hi_row[t]);
-  }
-  return ok;
+__device__ __forceinline__ void load_exp(Expansion<BD_CAP>& e, const ExpStore& s) {
+#pragma unroll
+  for (int k = 0; k < BD_CAP; ++k) e.p[k] = s.p[k];
+  e.n = s.n;
+}
+__device__ __forceinline__ void store_exp(ExpStore& s, const Expansion<BD_CAP>& e) {
+#pragma unroll
+  for (int k = 0; k < BD_CAP; ++k) s.p[k] = e.p[k];
+  s.n = e.n;
+}
+
+// v on the 2^-48 grid with |v * 2^48| <= 2^55 -> exact int64 (sums of <= 64 stay exact)
+__device__ __forceinline__ bool to_fixed(double v, long long& q) {
+  const double x = __dmul_rn(v, BD_FX_SCALE);
+  if (!(fabs(x) <= BD_FX_LIMIT) || x != rint(x)) return false;
+  q = __double2ll_rn(x);
+  return true;
 }
 
 // ----------------------------------------------------------------- cell source
+// 16-byte vector of token elements -> float64 dot with a float64 slice
 template <typename T>
-__device__ __forceinline__ double dot_token(const T* __restrict__ e, const double* __restrict__ q, int dim) {
+__device__ __forceinline__ double vec_dot(const uint4& v, const double* q) {
+  constexpr int PER = 16 / sizeof(T);
+  const T* x = reinterpret_cast<const T*>(&v);
   double acc = 0.0;
-  for (int k = 0; k < dim; ++k) acc = fma(Elem<T>::to_d(e[k]), q[k], acc);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) acc = fma(Elem<T>::to_d(x[k]), q[k], acc);
   return acc;
 }
 
+// Dot products of a range of document tokens with one query token, spread
+// over `G`-lane groups: lane `sub` of a group owns 16-byte vectors
+// sub, sub+G, ... of every token row (VPL of them), keeps the matching query
+// slice in registers, and the group sums with log2(G) shuffles. Tokens are
+// processed B at a time with every load issued before any arithmetic. Group
+// `gid` handles tokens j0 + gid + k * ngroups; the trip count is kept
+// warp-uniform (every lane of a warp runs the shuffles together).
+template <typename T, int G, int VPL, int B>
+__device__ __forceinline__ double tokens_max_dot(const T* __restrict__ dtok, int64_t j0, int64_t j1, const T* q,
+                                                 int dim, int gid, int ngroups, int sub, double init) {
+  constexpr int PER = 16 / sizeof(T);
+  constexpr int GPW = 32 / G;  // groups per warp
+  const int nvec = dim / PER;
+  double qs[VPL][PER];
+#pragma unroll
+  for (int u = 0; u < VPL; ++u) {
+    const int v = sub + u * G;
+    if (v < nvec) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(q) + v);
+      const T* x = reinterpret_cast<const T*>(&w);
+#pragma unroll
+      for (int k = 0; k < PER; ++k) qs[u][k] = Elem<T>::to_d(x[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < PER; ++k) qs[u][k] = 0.0;
+    }
+  }
+  double best = init;
+  const int gw = gid - gid % GPW;  // first group of this warp
+  for (int64_t jw = j0 + gw; jw < j1; jw += (int64_t)ngroups * B) {
+    const int64_t jb = jw + gid % GPW;
+    uint4 buf[B][VPL];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int64_t j = jb + (int64_t)b * ngroups;
+#pragma unroll
+      for (int u = 0; u < VPL; ++u) {
+        const int v = sub + u * G;
+        if (j < j1 && v < nvec) buf[b][u] = __ldg(reinterpret_cast<const uint4*>(dtok + j * dim) + v);
+        else buf[b][u] = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      double acc = 0.0;
+#pragma unroll
+      for (int u = 0; u < VPL; ++u) acc += vec_dot<T>(buf[b][u], qs[u]);
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const int64_t j = jb + (int64_t)b * ngroups;
+      if (j < j1) best = acc > best ? acc : best;
+    }
+  }
+  return best;
+}
+
 // ----------------------------------------------------------------- the kernel
-template <typename T>
-__global__ void __launch_bounds__(BD_THREADS) bandit_kernel(const BanditParams P) {
+template <typename T, int G, int VPL>
+__global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParams P) {
   extern __shared__ __align__(16) uint8_t bd_smem[];
+  constexpr int NGROUPS = BD_THREADS / G;
+  constexpr int B = VPL == 1 ? 8 : (VPL == 2 ? 4 : 2);
+  constexpr int GW = G <= 32 ? G : 32;
   const cbx_bandit_run_desc R = P.runs[blockIdx.x];
   const int N = R.n_rows, TC = R.n_cols, K = R.k;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = tid / G, sub = tid % G;
   const bool uniform = R.bounds_off < 0;
   const double* lo_b = uniform ? nullptr : P.bounds_lo + R.bounds_off;
   const double* hi_b = uniform ? nullptr : P.bounds_hi + R.bounds_off;
   const bool tokens = P.q_tokens != nullptr;
   const int dim = P.dim;
 
-  // shared layout: control block, reduction scratch, query row, [ranking arrays]
   struct Ctrl {
     int action;       // 0 reveal, 1 stop, 2 warm-up, 3 exhaustion, 4 error
     int i_star, t_star;
     int status;
     int64_t n_reveals;
     int iterations;
-    KeyIdx sel[4];
+    int pad;
+    unsigned long long cellkey;
+    int32_t swap_in, swap_out;  // best non-member / worst member of the last selection
   };
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(bd_smem);
-  KeyIdx* red = reinterpret_cast<KeyIdx*>(bd_smem + 128);            // [4][BD_WARPS]
-  double* cellred = reinterpret_cast<double*>(red + 4 * BD_WARPS);    // [BD_WARPS]
-  double* qrow = cellred + BD_WARPS;                                  // [dim] (token source)
-  uint8_t* rank_base = reinterpret_cast<uint8_t*>(qrow + (tokens ? dim : 0));
-  double *proxy, *lcb, *ucb;
-  uint8_t* member;
-  if (P.use_smem) {
-    proxy = reinterpret_cast<double*>(rank_base);
-    lcb = proxy + N;
-    ucb = lcb + N;
-    member = reinterpret_cast<uint8_t*>(ucb + N);
-  } else {
-    proxy = P.g_rank + R.state_off * 3;
-    lcb = proxy + N;
-    ucb = lcb + N;
-    member = P.g_member + R.state_off;
-  }
-  RowState* rows = P.rows + R.state_off;
+  Cand* red = reinterpret_cast<Cand*>(bd_smem + 128);                 // [4][BD_WARPS]
+  double* sq_log = reinterpret_cast<double*>(red + 4 * BD_WARPS);     // [BD_MAX_T + 1]
+  double* sq_rho = sq_log + BD_MAX_T + 1;                             // [BD_MAX_T + 1]
+  uint8_t* row_base = reinterpret_cast<uint8_t*>(sq_rho + BD_MAX_T + 1);
+  if (!P.use_smem) row_base = P.g_rows + (size_t)R.state_off * ROW_BYTES;
+  RowsView rv;
+  rv.carve(row_base, N);
+  ExpStore* g_obs = P.g_obs + R.state_off;
+  ExpStore* g_lo = P.g_lo + R.state_off;
+  ExpStore* g_hi = P.g_hi + R.state_off;
   int32_t* tr_i = P.trace_i + R.trace_off;
   int32_t* tr_t = P.trace_t + R.trace_off;
   double* tr_v = P.trace_v + R.trace_off;
 
-  // query / document geometry for the token source
   const T* qtok = nullptr;
   const T* dtok = nullptr;
   const int64_t* dto = nullptr;
@@ -267,107 +360,164 @@ __global__ void __launch_bounds__(BD_THREADS) bandit_kernel(const BanditParams P
   }
   const double init_cell = P.clamp_negative ? 0.0 : -INFINITY;
 
-  // cell value H[i, t]: block-cooperative for the token source
-  auto cell_block = [&](int i, int t) -> double {
-    if (!tokens) return P.matrix[(R.row_begin + i) * P.ld_matrix + t];
-    for (int k = tid; k < dim; k += BD_THREADS) qrow[k] = Elem<T>::to_d(qtok[(int64_t)t * dim + k]);
-    __syncthreads();
-    const int64_t j0 = dto[i], j1 = dto[i + 1];
-    double best = init_cell;
-    for (int64_t j = j0 + tid; j < j1; j += BD_THREADS) {
-      const double d = dot_token<T>(dtok + j * dim, qrow, dim);
-      best = d > best ? d : best;
+  // exact sum of a row's revealed values, rounded like math.fsum
+  auto obs_sum = [&](int i) -> double {
+    if (rv.exp_mode[i]) {
+      Expansion<BD_CAP> e;
+      load_exp(e, g_obs[i]);
+      return e.round();
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double w = __shfl_xor_sync(0xffffffffu, best, o);
-      best = w > best ? w : best;
+    return __dmul_rn(__ll2double_rn(rv.fx[i]), BD_FX_INV);
+  };
+  // add v to row i's exact sum; false on expansion overflow
+  auto obs_add = [&](int i, double v) -> bool {
+    long long q;
+    if (!rv.exp_mode[i]) {
+      if (to_fixed(v, q)) {
+        rv.fx[i] += q;
+        return true;
+      }
+      // leave the grid: the int64 sum becomes an exact two-term expansion
+      const long long f = rv.fx[i];
+      const double hi = __ll2double_rn(f);
+      const double lo = __ll2double_rn(f - __double2ll_rn(hi));
+      Expansion<BD_CAP> e;
+      e.clear();
+      bool ok = e.add(__dmul_rn(lo, BD_FX_INV));
+      ok &= e.add(__dmul_rn(hi, BD_FX_INV));
+      ok &= e.add(v);
+      store_exp(g_obs[i], e);
+      rv.exp_mode[i] = 1;
+      return ok;
     }
-    if (lane == 0) cellred[warp] = best;
-    __syncthreads();
-    double m = cellred[0];
-    for (int w = 1; w < BD_WARPS; ++w) m = cellred[w] > m ? cellred[w] : m;
-    __syncthreads();
-    return m;
+    Expansion<BD_CAP> e;
+    load_exp(e, g_obs[i]);
+    const bool ok = e.add(v);
+    store_exp(g_obs[i], e);
+    return ok;
   };
 
-  // cell value computed by one warp (warm-up: many rows in parallel)
+  // ledger._record (oracle.py:305-314) + refresh(i) (bandit.py:220-247) for one row
+  auto reveal_update = [&](int i, int t, double v) -> bool {
+    const int n = rv.cnt[i] + 1;
+    double mean = rv.mean[i], m2 = rv.m2[i];
+    const double d = __dsub_rn(v, mean);
+    mean = __dadd_rn(mean, __ddiv_rn(d, (double)n));
+    m2 = __dadd_rn(m2, __dmul_rn(d, __dsub_rn(v, mean)));
+    bool ok = obs_add(i, v);
+    const double obs = obs_sum(i);
+    rv.mean[i] = mean;
+    rv.m2[i] = m2;
+    rv.unrev[i] &= ~(1ull << t);
+    rv.cnt[i] = n;
+    double lo_sum, hi_sum;
+    if (uniform) {
+      // fsum of (T - n) copies of a constant == the correctly rounded product
+      lo_sum = (TC - n) ? __dmul_rn((double)(TC - n), R.lo_uniform) : 0.0;
+      hi_sum = (TC - n) ? __dmul_rn((double)(TC - n), R.hi_uniform) : 0.0;
+    } else {
+      Expansion<BD_CAP> x;
+      load_exp(x, g_lo[i]);
+      ok &= x.add(-lo_b[(int64_t)i * TC + t]);
+      store_exp(g_lo[i], x);
+      lo_sum = x.round();
+      load_exp(x, g_hi[i]);
+      ok &= x.add(-hi_b[(int64_t)i * TC + t]);
+      store_exp(g_hi[i], x);
+      hi_sum = x.round();
+    }
+    double px, l, u;
+    row_interval(n, m2, obs, lo_sum, hi_sum, TC, R.alpha_ef, sq_log, sq_rho, px, l, u);
+    rv.proxy[i] = px;
+    rv.lcb[i] = l;
+    rv.ucb[i] = u;
+    return ok;
+  };
+
+  // H[i, t] by one warp (warm-up cells)
   auto cell_warp = [&](int i, int t) -> double {
     if (!tokens) return P.matrix[(R.row_begin + i) * P.ld_matrix + t];
-    const T* q = qtok + (int64_t)t * dim;
-    const int64_t j0 = dto[i], j1 = dto[i + 1];
-    double best = init_cell;
-    for (int64_t j = j0 + lane; j < j1; j += 32) {
-      const T* e = dtok + j * dim;
-      double acc = 0.0;
-      for (int k = 0; k < dim; ++k) acc = fma(Elem<T>::to_d(e[k]), Elem<T>::to_d(q[k]), acc);
-      best = acc > best ? acc : best;
-    }
+    double best = tokens_max_dot<T, GW, VPL, (VPL == 1 ? 4 : 2)>(dtok, dto[i], dto[i + 1], qtok + (int64_t)t * dim,
+                                                                   dim, lane / GW, 32 / GW, lane % GW, init_cell);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 16; o >= GW; o >>= 1) {
       const double w = __shfl_xor_sync(0xffffffffu, best, o);
       best = w > best ? w : best;
     }
     return best;
   };
 
-  auto refresh = [&](int i, const RowState& s) {
-    double px, l, u;
-    row_interval(s, TC, uniform, R.lo_uniform, R.hi_uniform, R.alpha_ef, R.log_term, px, l, u);
-    proxy[i] = px;
-    lcb[i] = l;
-    ucb[i] = u;
-  };
-
   // rebuild(): membership = first K rows of the (-proxy, i) order (bandit.py:251-263)
   auto rebuild = [&]() {
-    for (int i = tid; i < N; i += BD_THREADS) member[i] = 0;
+    for (int i = tid; i < N; i += BD_THREADS) rv.member[i] = 0;
     __syncthreads();
     for (int r = 0; r < K; ++r) {
-      KeyIdx best{0.0, -1};
-      for (int i = tid; i < N; i += BD_THREADS) {
-        if (member[i]) continue;
-        KeyIdx c{proxy[i], i};
-        if (prefer(SEL_MAX_PROXY, c, best)) best = c;
-      }
-      warp_select(SEL_MAX_PROXY, best);
-      if (lane == 0) red[warp] = best;
+      Cand c{0, TIE_EMPTY};
+      for (int i = tid; i < N; i += BD_THREADS)
+        if (!rv.member[i]) cand_take(c, ord_key(rv.proxy[i]), (uint32_t)i);
+      c = warp_best(c);
+      if (lane == 0) red[warp] = c;
       __syncthreads();
-      if (tid == 0) {
-        KeyIdx b = red[0];
-        for (int w = 1; w < BD_WARPS; ++w)
-          if (prefer(SEL_MAX_PROXY, red[w], b)) b = red[w];
-        member[b.i] = 1;
+      if (warp == 0) {
+        Cand b = lane < BD_WARPS ? red[lane] : Cand{0, TIE_EMPTY};
+        b = warp_best(b);
+        if (lane == 0) rv.member[b.tie] = 1;
       }
       __syncthreads();
     }
   };
 
   // ------------------------------------------------------------ initial state (all n = 0)
-  const uint64_t full_mask = TC >= 64 ? ~0ull : ((1ull << TC) - 1ull);
-  for (int i = tid; i < N; i += BD_THREADS) {
-    RowState s;
-    s.mean = 0.0;
-    s.m2 = 0.0;
-    s.unrev = full_mask;
-    s.n = 0;
-    s.pad = 0;
-    s.obs.clear();
-    s.lo_un.clear();
-    s.hi_un.clear();
-    if (!uniform) {
-      for (int t = 0; t < TC; ++t) {
-        s.lo_un.add(lo_b[(int64_t)i * TC + t]);
-        s.hi_un.add(hi_b[(int64_t)i * TC + t]);
-      }
-    }
-    rows[i] = s;
-    refresh(i, s);
-  }
   if (tid == 0) {
     ctrl->status = 0;
     ctrl->n_reveals = 0;
     ctrl->iterations = 0;
+  }
+  for (int n = tid; n <= BD_MAX_T; n += BD_THREADS) {
+    double a = 0.0, b = 0.0;
+    if (n >= 1 && n <= TC) {
+      a = __dsqrt_rn(__ddiv_rn(__dmul_rn(2.0, R.log_term), (double)n));
+      double rho;
+      if (2 * n <= TC) rho = __dsub_rn(1.0, __ddiv_rn((double)(n - 1), (double)TC));
+      else rho = __dmul_rn(__dsub_rn(1.0, __ddiv_rn((double)n, (double)TC)), __dadd_rn(1.0, __ddiv_rn(1.0, (double)n)));
+      b = __dsqrt_rn(rho);
+    }
+    sq_log[n] = a;
+    sq_rho[n] = b;
+  }
+  __syncthreads();
+  const uint64_t full_mask = TC >= 64 ? ~0ull : ((1ull << TC) - 1ull);
+  for (int i = tid; i < N; i += BD_THREADS) {
+    rv.mean[i] = 0.0;
+    rv.m2[i] = 0.0;
+    rv.fx[i] = 0;
+    rv.exp_mode[i] = 0;
+    rv.unrev[i] = full_mask;
+    rv.cnt[i] = 0;
+    double lo_sum, hi_sum;
+    if (uniform) {
+      lo_sum = __dmul_rn((double)TC, R.lo_uniform);
+      hi_sum = __dmul_rn((double)TC, R.hi_uniform);
+    } else {
+      Expansion<BD_CAP> a, b;
+      a.clear();
+      b.clear();
+      bool ok = true;
+      for (int t = 0; t < TC; ++t) {
+        ok &= a.add(lo_b[(int64_t)i * TC + t]);
+        ok &= b.add(hi_b[(int64_t)i * TC + t]);
+      }
+      if (!ok) ctrl->status = 2;
+      store_exp(g_lo[i], a);
+      store_exp(g_hi[i], b);
+      lo_sum = a.round();
+      hi_sum = b.round();
+    }
+    double px, l, u;
+    row_interval(0, 0.0, 0.0, lo_sum, hi_sum, TC, R.alpha_ef, sq_log, sq_rho, px, l, u);
+    rv.proxy[i] = px;
+    rv.lcb[i] = l;
+    rv.ucb[i] = u;
   }
   __syncthreads();
   rebuild();
@@ -383,91 +533,107 @@ __global__ void __launch_bounds__(BD_THREADS) bandit_kernel(const BanditParams P
   const double eps = R.explore_mode == CBX_UNIFORM_ROW ? 1.0 : R.epsilon;
   const int64_t total_cells = (int64_t)N * TC;
   int term = CBX_TERM_SEPARATION;
+  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long tc0 = clock64(), tcs = tc0;
+#define BD_PHASE(k)                            \
+  do {                                         \
+    if (P.prof && tid == 0) {                  \
+      const unsigned long long _n = clock64(); \
+      ph[k] += _n - tc0;                       \
+      tc0 = _n;                                \
+    }                                          \
+  } while (0)
 
   while (true) {
+    BD_PHASE(3);
     // ---------------------------------------------------------- boundary selection
-    KeyIdx acc[4];
-#pragma unroll
-    for (int s = 0; s < 4; ++s) acc[s] = KeyIdx{0.0, -1};
-    for (int i = tid; i < N; i += BD_THREADS) {
-      if (member[i]) {
-        KeyIdx a{lcb[i], i}, b{proxy[i], i};
-        if (prefer(SEL_MIN_LCB, a, acc[0])) acc[0] = a;
-        if (prefer(SEL_WORST_PROXY, b, acc[3])) acc[3] = b;
-      } else {
-        KeyIdx a{ucb[i], i}, b{proxy[i], i};
-        if (prefer(SEL_MAX_UCB, a, acc[1])) acc[1] = a;
-        if (prefer(SEL_MAX_PROXY, b, acc[2])) acc[2] = b;
+    {
+      Cand c[4] = {{0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}};
+      for (int i = tid; i < N; i += BD_THREADS) {
+        const uint64_t pk = ord_key(rv.proxy[i]);
+        if (rv.member[i]) {
+          cand_take(c[0], ~ord_key(rv.lcb[i]), (uint32_t)i);
+          cand_take(c[3], ~pk, ~(uint32_t)i);
+        } else {
+          cand_take(c[1], ord_key(rv.ucb[i]), (uint32_t)i);
+          cand_take(c[2], pk, (uint32_t)i);
+        }
       }
-    }
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      warp_select(s, acc[s]);
-      if (lane == 0) red[s * BD_WARPS + warp] = acc[s];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      KeyIdx f[4];
       for (int s = 0; s < 4; ++s) {
-        f[s] = red[s * BD_WARPS];
-        for (int w = 1; w < BD_WARPS; ++w)
-          if (prefer(s, red[s * BD_WARPS + w], f[s])) f[s] = red[s * BD_WARPS + w];
-        ctrl->sel[s] = f[s];
+        const Cand w = warp_best(c[s]);
+        if (lane == 0) red[s * BD_WARPS + warp] = w;
       }
-      ctrl->iterations += 1;
-      const int i_plus = f[0].i, i_minus = f[1].i;
-      const double ucb_minus = i_minus >= 0 ? f[1].k : -INFINITY;
-      int action;
-      if (lcb[i_plus] >= ucb_minus) {
-        action = 1;
-      } else if (!warmed) {
-        action = 2;
-        warmed = true;
-      } else if (ctrl->n_reveals == total_cells) {
-        action = 3;
-      } else {
-        action = 0;
-        const double wp = __dsub_rn(ucb[i_plus], lcb[i_plus]);
-        const double wm = __dsub_rn(ucb[i_minus], lcb[i_minus]);
-        int i_star = wp >= wm ? i_plus : i_minus;
-        uint64_t un = rows[i_star].unrev;
-        if (!un) {
-          i_star = i_star == i_plus ? i_minus : i_plus;
-          un = rows[i_star].unrev;
-          if (!un) {
-            action = 4;
-            ctrl->status = 1;
-          }
-        }
-        if (action == 0) {
-          int t_star = -1;
-          if (rng.random() < eps) {
-            uint32_t pos = rng.integers((uint32_t)__popcll(un));
-            uint64_t m = un;
-            for (uint32_t q = 0; q < pos; ++q) m &= m - 1;  // drop the lowest `pos` set bits
-            t_star = __ffsll((long long)m) - 1;
-          } else if (uniform) {
-            t_star = __ffsll((long long)un) - 1;  // all widths equal: first unrevealed column
-          } else {
-            // first argmax of the width over the ascending unrevealed columns
-            double best = -INFINITY;
-            for (int t = 0; t < TC; ++t) {
-              if (!((un >> t) & 1ull)) continue;
-              const double w = __dsub_rn(hi_b[(int64_t)i_star * TC + t], lo_b[(int64_t)i_star * TC + t]);
-              if (w > best) {
-                best = w;
-                t_star = t;
-              }
-            }
-            if (t_star < 0) t_star = __ffsll((long long)un) - 1;
-          }
-          ctrl->i_star = i_star;
-          ctrl->t_star = t_star;
-        }
-      }
-      ctrl->action = action;
     }
     __syncthreads();
+    BD_PHASE(0);
+    if (warp == 0) {
+      Cand f[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) f[s] = warp_best(lane < BD_WARPS ? red[s * BD_WARPS + lane] : Cand{0, TIE_EMPTY});
+      if (lane == 0) {
+        ctrl->iterations += 1;
+        ctrl->swap_in = f[2].key ? (int)f[2].tie : -1;
+        ctrl->swap_out = f[3].key ? (int)~f[3].tie : -1;
+        const int i_plus = (int)f[0].tie;
+        const int i_minus = f[1].key ? (int)f[1].tie : -1;
+        const double lcb_plus = rv.lcb[i_plus];
+        const double ucb_minus = i_minus >= 0 ? rv.ucb[i_minus] : -INFINITY;
+        int action;
+        if (lcb_plus >= ucb_minus) {
+          action = 1;
+        } else if (!warmed) {
+          action = 2;
+          warmed = true;
+        } else if (ctrl->n_reveals == total_cells) {
+          action = 3;
+        } else {
+          action = 0;
+          const double wp = __dsub_rn(rv.ucb[i_plus], lcb_plus);
+          const double wm = __dsub_rn(ucb_minus, rv.lcb[i_minus]);
+          int i_star = wp >= wm ? i_plus : i_minus;
+          uint64_t un = rv.unrev[i_star];
+          if (!un) {
+            i_star = i_star == i_plus ? i_minus : i_plus;
+            un = rv.unrev[i_star];
+            if (!un) {
+              action = 4;
+              ctrl->status = 1;
+            }
+          }
+          if (action == 0) {
+            int t_star;
+            if (rng.random() < eps) {
+              uint32_t pos = rng.integers((uint32_t)__popcll(un));
+              uint64_t m = un;
+              for (uint32_t q = 0; q < pos; ++q) m &= m - 1;  // drop the lowest `pos` set bits
+              t_star = __ffsll((long long)m) - 1;
+            } else if (uniform) {
+              t_star = __ffsll((long long)un) - 1;  // all widths equal: first unrevealed column
+            } else {
+              // first argmax of the width over the ascending unrevealed columns
+              double best = -INFINITY;
+              t_star = -1;
+              for (int t = 0; t < TC; ++t) {
+                if (!((un >> t) & 1ull)) continue;
+                const double w = __dsub_rn(hi_b[(int64_t)i_star * TC + t], lo_b[(int64_t)i_star * TC + t]);
+                if (w > best) {
+                  best = w;
+                  t_star = t;
+                }
+              }
+              if (t_star < 0) t_star = __ffsll((long long)un) - 1;
+            }
+            ctrl->i_star = i_star;
+            ctrl->t_star = t_star;
+            ctrl->cellkey = ord_key(init_cell);
+          }
+        }
+        ctrl->action = action;
+      }
+    }
+    __syncthreads();
+    BD_PHASE(1);
     const int action = ctrl->action;
     if (action == 1) break;
     if (action == 3) {
@@ -479,7 +645,7 @@ __global__ void __launch_bounds__(BD_THREADS) bandit_kernel(const BanditParams P
     if (action == 2) {
       // -------------------------------------------------------- lazy warm-up (bandit.py:285-296)
       warmed = true;
-      int64_t base = ctrl->n_reveals;
+      const int64_t base = ctrl->n_reveals;
       int64_t m;
       if (R.explore_mode == CBX_EPSILON_GREEDY) {
         m = N;
@@ -488,6 +654,18 @@ __global__ void __launch_bounds__(BD_THREADS) bandit_kernel(const BanditParams P
             tr_i[base + i] = i;
             tr_t[base + i] = (int32_t)rng.integers((uint32_t)TC);
           }
+        __syncthreads();
+        // one warp per document: every token once, dotted with the row's warm-up query token
+        for (int i = warp; i < N; i += BD_WARPS) {
+          const double v = cell_warp(i, tr_t[base + i]);
+          if (lane == 0) rv.wkey[i] = ord_key(v);
+        }
+        __syncthreads();
+        for (int i = tid; i < N; i += BD_THREADS) {
+          const double v = ord_val(rv.wkey[i]);
+          tr_v[base + i] = v;
+          if (!reveal_update(i, tr_t[base + i], v)) ctrl->status = 2;
+        }
       } else {
         m = R.n_warm;
         const int32_t* wc = P.warm_cells + R.warm_off;
@@ -495,72 +673,65 @@ __global__ void __launch_bounds__(BD_THREADS) bandit_kernel(const BanditParams P
           tr_i[base + s] = wc[s] / TC;
           tr_t[base + s] = wc[s] % TC;
         }
-      }
-      __syncthreads();
-      for (int64_t s = warp; s < m; s += BD_WARPS) {
-        const double v = cell_warp(tr_i[base + s], tr_t[base + s]);
-        if (lane == 0) tr_v[base + s] = v;
-      }
-      __syncthreads();
-      if (R.explore_mode == CBX_EPSILON_GREEDY) {
-        for (int i = tid; i < N; i += BD_THREADS) {
-          RowState s = rows[i];
-          if (!record(s, tr_t[base + i], tr_v[base + i], uniform, uniform ? nullptr : lo_b + (int64_t)i * TC,
-                      uniform ? nullptr : hi_b + (int64_t)i * TC))
-            ctrl->status = 2;
-          rows[i] = s;
-        }
-      } else if (tid == 0) {
-        for (int64_t s2 = 0; s2 < m; ++s2) {
-          const int i = tr_i[base + s2];
-          RowState s = rows[i];
-          if (!record(s, tr_t[base + s2], tr_v[base + s2], uniform, uniform ? nullptr : lo_b + (int64_t)i * TC,
-                      uniform ? nullptr : hi_b + (int64_t)i * TC))
-            ctrl->status = 2;
-          rows[i] = s;
-        }
-      }
-      __syncthreads();
-      if (m > 0) {
-        for (int i = tid; i < N; i += BD_THREADS) refresh(i, rows[i]);
         __syncthreads();
-        rebuild();
+        for (int64_t s = warp; s < m; s += BD_WARPS) {
+          const double v = cell_warp(tr_i[base + s], tr_t[base + s]);
+          if (lane == 0) tr_v[base + s] = v;
+        }
+        __syncthreads();
+        if (tid == 0)
+          for (int64_t s2 = 0; s2 < m; ++s2)
+            if (!reveal_update(tr_i[base + s2], tr_t[base + s2], tr_v[base + s2])) ctrl->status = 2;
       }
+      __syncthreads();
+      if (m > 0) rebuild();
       if (tid == 0) ctrl->n_reveals = base + m;
       __syncthreads();
+      BD_PHASE(4);
       continue;
     }
 
     // ---------------------------------------------------------- reveal one cell
     const int i_star = ctrl->i_star, t_star = ctrl->t_star;
-    const double v0 = cell_block(i_star, t_star);
+    if (tokens) {
+      double best = tokens_max_dot<T, G, VPL, B>(dtok, dto[i_star], dto[i_star + 1], qtok + (int64_t)t_star * dim, dim,
+                                                 gid, NGROUPS, sub, init_cell);
+#pragma unroll
+      for (int o = 16; o >= G; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, best, o);
+        best = w > best ? w : best;
+      }
+      if (lane == 0) atomicMax(&ctrl->cellkey, (unsigned long long)ord_key(best));
+      __syncthreads();
+    }
+    BD_PHASE(2);
     if (tid == 0) {
-      double v = v0;
-      if (!tokens) v = P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
+      const double v = tokens ? ord_val(ctrl->cellkey) : P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
       const int64_t pos = ctrl->n_reveals;
       tr_i[pos] = i_star;
       tr_t[pos] = t_star;
       tr_v[pos] = v;
       ctrl->n_reveals = pos + 1;
-      RowState s = rows[i_star];
-      if (!record(s, t_star, v, uniform, uniform ? nullptr : lo_b + (int64_t)i_star * TC,
-                  uniform ? nullptr : hi_b + (int64_t)i_star * TC))
-        ctrl->status = 2;
-      rows[i_star] = s;
-      refresh(i_star, s);
+      if (!reveal_update(i_star, t_star, v)) ctrl->status = 2;
       // keep the Top-K set equal to the first K of the (-proxy, i) order
-      const KeyIdx me{proxy[i_star], i_star};
-      if (member[i_star]) {
-        const KeyIdx bnm = ctrl->sel[SEL_MAX_PROXY];
-        if (bnm.i >= 0 && prefer(SEL_MAX_PROXY, bnm, me)) {
-          member[i_star] = 0;
-          member[bnm.i] = 1;
+      const uint64_t mk = ord_key(rv.proxy[i_star]);
+      if (rv.member[i_star]) {
+        const int b = ctrl->swap_in;  // best non-member
+        if (b >= 0) {
+          const uint64_t bk = ord_key(rv.proxy[b]);
+          if (bk > mk || (bk == mk && b < i_star)) {
+            rv.member[i_star] = 0;
+            rv.member[b] = 1;
+          }
         }
       } else {
-        const KeyIdx wm = ctrl->sel[SEL_WORST_PROXY];
-        if (wm.i >= 0 && prefer(SEL_MAX_PROXY, me, wm)) {
-          member[i_star] = 1;
-          member[wm.i] = 0;
+        const int w = ctrl->swap_out;  // worst member
+        if (w >= 0) {
+          const uint64_t wk = ord_key(rv.proxy[w]);
+          if (mk > wk || (mk == wk && i_star < w)) {
+            rv.member[i_star] = 1;
+            rv.member[w] = 0;
+          }
         }
       }
     }
@@ -572,14 +743,13 @@ __global__ void __launch_bounds__(BD_THREADS) bandit_kernel(const BanditParams P
     int32_t* out_k = P.topk + (int64_t)blockIdx.x * P.max_k;
     int cnt = 0;
     for (int i = 0; i < N && cnt < K; ++i) {
-      if (!member[i]) continue;
-      // insertion sort by (-proxy, i)
+      if (!rv.member[i]) continue;
       int p = cnt++;
-      const KeyIdx me{proxy[i], i};
+      const uint64_t mk = ord_key(rv.proxy[i]);
       while (p > 0) {
         const int o = out_k[p - 1];
-        const KeyIdx other{proxy[o], o};
-        if (!prefer(SEL_MAX_PROXY, me, other)) break;
+        const uint64_t ok = ord_key(rv.proxy[o]);
+        if (!(mk > ok || (mk == ok && i < o))) break;
         out_k[p] = o;
         --p;
       }
@@ -592,18 +762,62 @@ __global__ void __launch_bounds__(BD_THREADS) bandit_kernel(const BanditParams P
     o.status = ctrl->status;
     o.pad = 0;
     P.out[blockIdx.x] = o;
+    if (P.prof) {
+      ph[5] = clock64() - tcs;
+      for (int k = 0; k < 6; ++k) P.prof[blockIdx.x * 8 + k] = ph[k];
+    }
   }
+#undef BD_PHASE
 }
 
 }  // namespace cbx
 
 using namespace cbx;
 
+static unsigned long long* g_bandit_prof = nullptr;
+
+static size_t state_parts(int64_t rows, size_t* off_obs, size_t* off_lo, size_t* off_hi, size_t* off_rows) {
+  size_t o = 0;
+  *off_obs = o;
+  o += align_up(sizeof(ExpStore) * (size_t)rows, 256);
+  *off_lo = o;
+  o += align_up(sizeof(ExpStore) * (size_t)rows, 256);
+  *off_hi = o;
+  o += align_up(sizeof(ExpStore) * (size_t)rows, 256);
+  *off_rows = o;
+  o += align_up(ROW_BYTES * (size_t)rows + 64, 256);
+  return o;
+}
+
+template <typename T, int G, int VPL>
+static int launch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, cudaStream_t st) {
+  auto kern = bandit_kernel<T, G, VPL>;
+  CBX_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)n_runs, BD_THREADS, smem, st>>>(P);
+  CBX_LAUNCH_CHECK("bandit_kernel launch");
+  return CBX_OK;
+}
+
+// lanes per token row: one 16-byte vector each, up to a warp; longer rows give lanes several vectors
+template <typename T>
+static int dispatch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, cudaStream_t st, int dim) {
+  constexpr int PER = 16 / sizeof(T);
+  const int nvec = dim / PER;
+  if (nvec <= 8) return launch_bandit<T, 8, 1>(P, n_runs, smem, st);
+  if (nvec <= 16) return launch_bandit<T, 16, 1>(P, n_runs, smem, st);
+  if (nvec <= 32) return launch_bandit<T, 32, 1>(P, n_runs, smem, st);
+  if (nvec <= 64) return launch_bandit<T, 32, 2>(P, n_runs, smem, st);
+  if (nvec <= 128) return launch_bandit<T, 32, 4>(P, n_runs, smem, st);
+  return fail(CBX_EINVAL, "bandit: embedding rows above 2 KiB are not supported");
+}
+
 extern "C" {
 
+void cbx_bandit_set_profile(void* counters) { g_bandit_prof = static_cast<unsigned long long*>(counters); }
+
 size_t cbx_bandit_state_bytes(int64_t total_rows) {
-  return align_up(sizeof(RowState) * (size_t)total_rows, 256) + align_up(3 * sizeof(double) * total_rows, 256) +
-         align_up((size_t)total_rows, 256);
+  size_t a, b, c, d;
+  return state_parts(total_rows, &a, &b, &c, &d);
 }
 
 int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix, const cbx_bandit_run_desc* runs,
@@ -616,6 +830,22 @@ int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix, 
   if (!b && !matrix) return fail(CBX_EINVAL, "bandit: need token embeddings or a cell matrix");
   if (n_runs > 0x7FFFFFFF) return fail(CBX_EINVAL, "bandit: too many runs");
   if (max_rows <= 0) return fail(CBX_EINVAL, "bandit: max_rows must be positive");
+  if (b) {
+    const size_t es = dtype_size(b->dtype);
+    if ((b->dim * es) % 16 != 0) return fail(CBX_EINVAL, "bandit: token rows must be a multiple of 16 bytes");
+    if ((reinterpret_cast<uintptr_t>(b->d_tokens) | reinterpret_cast<uintptr_t>(b->q_tokens)) & 15)
+      return fail(CBX_EINVAL, "bandit: token buffers must be 16-byte aligned");
+  }
+  // recover the row capacity the caller sized the state for
+  int64_t lo = 0, hi = (int64_t)(state_bytes / 64) + 1;
+  while (lo < hi) {
+    int64_t mid = (lo + hi + 1) / 2;
+    if (cbx_bandit_state_bytes(mid) <= state_bytes) lo = mid;
+    else hi = mid - 1;
+  }
+  size_t o_obs, o_lo, o_hi, o_rows;
+  state_parts(lo, &o_obs, &o_lo, &o_hi, &o_rows);
+  uint8_t* base = static_cast<uint8_t*>(state);
   BanditParams P;
   P.q_tokens = b ? b->q_tokens : nullptr;
   P.q_tok_off = b ? b->q_tok_off : nullptr;
@@ -629,45 +859,30 @@ int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix, 
   P.bounds_lo = bounds_lo;
   P.bounds_hi = bounds_hi;
   P.warm_cells = warm_cells;
-  // state layout: RowState[total] | rank[3 * total] | member[total]; the caller sized it with
-  // cbx_bandit_state_bytes(total_rows) and gives each run a disjoint state_off range
-  const size_t row_sz = sizeof(RowState);
-  // recover total_rows from state_bytes (largest t with state_bytes(t) <= state_bytes)
-  int64_t lo = 0, hi = (int64_t)(state_bytes / row_sz) + 1;
-  while (lo < hi) {
-    int64_t mid = (lo + hi + 1) / 2;
-    if (cbx_bandit_state_bytes(mid) <= state_bytes) lo = mid;
-    else hi = mid - 1;
-  }
-  const int64_t total = lo;
-  uint8_t* base = static_cast<uint8_t*>(state);
-  P.rows = reinterpret_cast<RowState*>(base);
-  P.g_rank = reinterpret_cast<double*>(base + align_up(row_sz * (size_t)total, 256));
-  P.g_member = base + align_up(row_sz * (size_t)total, 256) + align_up(3 * sizeof(double) * total, 256);
+  P.g_obs = reinterpret_cast<ExpStore*>(base + o_obs);
+  P.g_lo = reinterpret_cast<ExpStore*>(base + o_lo);
+  P.g_hi = reinterpret_cast<ExpStore*>(base + o_hi);
+  P.g_rows = base + o_rows;
   P.topk = topk;
   P.max_k = max_k;
   P.trace_i = trace_i;
   P.trace_t = trace_t;
   P.trace_v = trace_v;
   P.out = out;
-  const int dim = b ? b->dim : 0;
-  size_t smem = 128 + sizeof(KeyIdx) * 4 * BD_WARPS + sizeof(double) * BD_WARPS + sizeof(double) * dim;
+  P.prof = g_bandit_prof;
+  size_t smem = 128 + sizeof(Cand) * 4 * BD_WARPS + 2 * sizeof(double) * (BD_MAX_T + 1);
   smem = align_up(smem, 16);
   P.use_smem = max_rows <= BD_SMEM_ROWS ? 1 : 0;
-  if (P.use_smem) smem += (size_t)max_rows * (3 * sizeof(double) + 1);
+  if (P.use_smem) smem += (size_t)max_rows * ROW_BYTES + 64;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int dt = b ? b->dtype : CBX_F64;
-  auto launch = [&](auto kern) -> int {
-    CBX_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)n_runs, BD_THREADS, smem, st>>>(P);
-    CBX_LAUNCH_CHECK("bandit_kernel launch");
-    return CBX_OK;
-  };
+  const int dim = b ? b->dim : 16;
   switch (dt) {
-    case CBX_F32: return launch(bandit_kernel<float>);
-    case CBX_F16: return launch(bandit_kernel<__half>);
-    case CBX_BF16: return launch(bandit_kernel<__nv_bfloat16>);
-    case CBX_F64: return launch(bandit_kernel<double>);
+    case CBX_F32: return dispatch_bandit<float>(P, n_runs, smem, st, dim);
+    case CBX_F16: return dispatch_bandit<__half>(P, n_runs, smem, st, dim);
+    case CBX_BF16: return dispatch_bandit<__nv_bfloat16>(P, n_runs, smem, st, dim);
+    case CBX_F64: return b ? dispatch_bandit<double>(P, n_runs, smem, st, dim)
+                           : launch_bandit<double, 8, 1>(P, n_runs, smem, st);
   }
   return fail(CBX_EINVAL, "bandit: unknown dtype");
 }
