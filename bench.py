@@ -1,23 +1,24 @@
 #!/usr/bin/env python
-"""Benchmark of the exhaustive MaxSim reranker (P1) — the driver's contract.
+"""Benchmark of the B200 MaxSim reranker — the driver's contract.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
 
-One "step" = one pass of the hot path over one batch: MaxSim scores of every
-candidate of every query (tcgen05 dense scorer) + per-query Top-K. The
-workload is BASELINE.json configs[1] ("cfg2": 256 queries x 1000 candidates,
-Lq = 32, d = 128, fp16, lognormal doc lengths, K = 10), drawn on the device
-(synthetic, seeded by rank). Inputs (11.7 GB of doc tokens) are larger than
-L2 (126 MB), so no flush is needed between steps.
+One "step" = one pass of the hot path over one batch: the MaxSim score of
+every candidate of every query (tcgen05 dense scorer, P1) + per-query Top-K.
+The workload is BASELINE.json configs[1] ("cfg2": 256 queries x 1000
+candidates, Lq = 32, d = 128, fp16, lognormal doc lengths, K = 10), drawn on
+the device (synthetic, seeded by rank). Inputs (11.7 GB of doc tokens)
+exceed L2 (126 MB), so no flush is needed between steps.
 
-metric: MaxSim cells/s (cell = one (document, query token) pair), plus
-queries/s and the scorer's achieved HBM GB/s against the measured peak.
+The JSON line also carries the Col-Bandit loop (P2) on the same batch
+("bandit": one CTA per query, default BanditConfig, seed (0, q)), with its
+revealed-cell throughput, gather bandwidth and CPU-oracle parity.
+
+``--impl reference`` times the reference's CPU algorithm (the oracle port in
+oracle/maxsim_ref: float64 GEMM + column max + math.fsum + lexsort) on the
+box's host cores, one process per core, for the same metric and config.
 Multi-GPU: one process per GPU, each with its own batch (weak scaling, no
 collective on the data path); value = all ranks' cells / max-over-ranks time.
-
-``--impl reference`` times the CPU oracle port (oracle/maxsim_ref — the
-reference's float64 GEMM + column max + math.fsum + lexsort, restated) on
-the box's host cores with one process per core, for the same metric/config.
 """
 
 from __future__ import annotations
@@ -25,7 +26,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -46,49 +46,94 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + clock-event reasons sampled through NVML every 5 ms during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self.error = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            self.nv = None
+            self.error = str(e)
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.samples.append((sm, reasons))
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                vals = [v.strip() for v in out.stdout.strip().split(",")]
-                if len(vals) == 6:
-                    self.samples.append(vals)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+                self._sample()
+            except Exception as e:  # pragma: no cover
+                self.error = str(e)
+                return
+            self._stop.wait(0.005)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self.nv is not None:
+            self._sample()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t is not None:
+            self._t.join(timeout=5)
+            try:
+                self._sample()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvml unavailable: {self.error}"]}
         import statistics
 
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        nv = self.nv
+        active = set()
+        for _, r in self.samples:
+            for name, attr in self.REASONS.items():
+                if r & getattr(nv, attr):
+                    active.add(name)
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_sm,
+                "reasons": sorted(active), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------- helpers
+def _query_host(batch, host_off, q):
+    """float64 copies of query q and its documents (for the CPU oracle)."""
+    qo, do, qd = host_off
+    d0, d1 = int(qd[q]), int(qd[q + 1])
+    qt = batch.q_tokens[int(qo[q]):int(qo[q + 1])].double().cpu().numpy()
+    dt = batch.d_tokens[int(do[d0]):int(do[d1])].double().cpu().numpy()
+    docs = [dt[int(do[i] - do[d0]):int(do[i + 1] - do[d0])] for i in range(d0, d1)]
+    return qt, docs
+
+
+def _blas_one_thread():
+    try:
+        from threadpoolctl import threadpool_limits
+
+        return threadpool_limits(1)
+    except Exception:  # pragma: no cover
+        return None
 
 
 # ---------------------------------------------------------------------------- our arm
@@ -96,9 +141,8 @@ def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
 
-    from paper_2602_02827_b200 import _lib
     from paper_2602_02827_b200 import workloads as W
-    from paper_2602_02827_b200.batch import HostBatch, maxsim_scores, rerank_topk, rerank_topk_host, topk
+    from paper_2602_02827_b200.batch import HostBatch, maxsim_scores, rerank_topk_host, topk
 
     torch.cuda.set_device(local_rank)
     cfg = W.CONFIGS[args.config]
@@ -107,10 +151,13 @@ def run_ours(args, rank, world, local_rank):
     nq, K = batch.n_queries, cfg.k
     elem = batch.d_tokens.element_size()
     qo, do, qd = host_off
-    cells_per_step = int(sum((qd[q + 1] - qd[q]) * (qo[q + 1] - qo[q]) for q in range(nq)))
+    lq = np.diff(qo)
+    ndocs = np.diff(qd)
+    qtok = do[qd[1:]] - do[qd[:-1]]
+    cells_per_step = int((ndocs * lq).sum())
     alg_bytes = int(batch.d_tokens.numel() * elem + batch.q_tokens.numel() * elem + 4 * batch.n_docs)
-    alg_flops = int(2 * sum((do[qd[q + 1]] - do[qd[q]]) * (qo[q + 1] - qo[q]) for q in range(nq)) * batch.dim)
-
+    alg_flops = int(2 * (qtok * lq).sum() * batch.dim)
+    hbm_peak, tf_peak, peak_kind = _peaks()
     stream = torch.cuda.current_stream()
     scores = torch.empty(batch.n_docs, dtype=torch.float32, device="cuda")
 
@@ -120,11 +167,12 @@ def run_ours(args, rank, world, local_rank):
         maxsim_scores(batch, out=scores)
         if ev is not None:
             ev[1].record(stream)
-        idx, val = topk(scores, batch.q_doc_off, K, batch.max_q_docs)
+        res = topk(scores, batch.q_doc_off, K, batch.max_q_docs)
         if ev is not None:
             ev[2].record(stream)
-        return idx, val
+        return res
 
+    # ------------------------------------------------ P1, device-resident inputs
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -141,81 +189,67 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    ms = start.elapsed_time(stop)
-    kern_ms = [e[0].elapsed_time(e[1]) for e in evs]
-    topk_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([start.elapsed_time(stop)], dtype=torch.float64, device="cuda")
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(t.item())
-    hbm_peak, tf_peak, peak_kind = _peaks()
+    ms_step = float(t.item()) / args.steps
+    kern_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    topk_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
 
     result = None
     if rank == 0:
-        ms_step = ms_max / args.steps
-        value = cells_per_step * world / (ms_step / 1e3)
-        kavg = sum(kern_ms) / len(kern_ms)
-        achieved = alg_bytes / (kavg / 1e3) / 1e9
+        achieved = alg_bytes / (kern_ms / 1e3) / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
             traffic = json.load(open(tpath)).get(args.config)
         result = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (device RNG, BASELINE.json configs[1] recipe)",
+            "metric": METRIC, "value": cells_per_step * world / (ms_step / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+            "data": "synthetic (device RNG, BASELINE.json configs[1] recipe)",
             "config": {"workload": f"{cfg.name}: {nq} queries x {cfg.n_docs} docs, Lq={cfg.lq[0]}, d={cfg.dim}, "
-                                   f"lognormal lengths (mean 180, sigma 0.5, clip [16,512]), K={K}",
+                                   f"lognormal lengths (mean 180, sigma 0.5, clip [16,512]), {cfg.dtype}, K={K}",
                        "queries_per_gpu": nq, "doc_tokens_per_gpu": int(batch.d_tokens.shape[0]),
-                       "l2": "inputs (%.1f GB) exceed L2; no flush" % (alg_bytes / 1e9),
+                       "l2": "inputs (%.1f GB) exceed L2 (126 MB); no flush" % (alg_bytes / 1e9),
                        "parallelism": f"query-sharded x{world} (no collective)"},
             "queries_per_s": nq * world / (ms_step / 1e3),
-            "scorer_ms": kavg, "topk_ms": sum(topk_ms) / len(topk_ms),
+            "scorer_ms": kern_ms, "topk_ms": topk_ms,
             "roofline": {"bound": "hbm", "kernel": "maxsim_tc_kernel", "achieved": achieved, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved / hbm_peak, "peak_kind": peak_kind,
                          "alg_bytes_per_launch": alg_bytes, "traffic": traffic,
-                         "tensor_tflops": alg_flops / (kavg / 1e3) / 1e12, "tensor_peak": tf_peak},
+                         "tensor_tflops": alg_flops / (kern_ms / 1e3) / 1e12, "tensor_peak": tf_peak},
             "clocks": clocks.summary(),
             "gpu_launches": args.steps * 2,
         }
 
-    # ------------------------------------------------ parity on a sample + CPU baseline (rank 0, N = 1)
+    # ------------------------------------------------ P1 parity on sampled queries + CPU baseline
     if rank == 0:
         from oracle import maxsim_ref
 
-        n_check = min(nq, args.check_queries)
-        idx_h = idx.cpu().numpy()
-        sc_h = scores.cpu().numpy()
-        ok = True
-        cpu_cells, cpu_s = 0, 0.0
-        try:
-            from threadpoolctl import threadpool_limits
-            lim = threadpool_limits(1)
-        except Exception:
-            lim = None
-        for q in range(n_check):
-            d0, d1 = int(qd[q]), int(qd[q + 1])
-            qt = batch.q_tokens[int(qo[q]):int(qo[q + 1])].double().cpu().numpy()
-            dt = batch.d_tokens[int(do[d0]):int(do[d1])].double().cpu().numpy()
-            docs = [dt[int(do[i] - do[d0]):int(do[i + 1] - do[d0])] for i in range(d0, d1)]
+        lim = _blas_one_thread()
+        idx_h, sc_h = idx.cpu().numpy(), scores.cpu().numpy()
+        ok, n_chk, cpu_cells, cpu_s = True, 0, 0, 0.0
+        for q in range(nq):
+            qt, docs = _query_host(batch, host_off, q)
             t0 = time.perf_counter()
             ref_s, ref_t, _ = maxsim_ref.score_query(qt, docs, K)
             cpu_s += time.perf_counter() - t0
-            cpu_cells += (d1 - d0) * qt.shape[0]
-            if not np.allclose(sc_h[d0:d1], ref_s, rtol=1e-3, atol=0):
-                ok = False
-            got = idx_h[q].tolist()
-            if got != ref_t:
-                for g_, r_ in zip(got, ref_t):
-                    if g_ != r_ and abs(ref_s[g_] - ref_s[r_]) > 1e-3 * abs(ref_s[r_]):
-                        ok = False
-        if lim is not None:
-            lim.unregister() if hasattr(lim, "unregister") else None
-        result["parity"] = {"queries_checked": n_check, "scores_rtol": 1e-3, "topk_match": ok}
+            cpu_cells += len(docs) * qt.shape[0]
+            d0 = int(qd[q])
+            ok &= bool(np.allclose(sc_h[d0:d0 + len(docs)], ref_s, rtol=1e-3, atol=0))
+            for g_, r_ in zip(idx_h[q].tolist(), ref_t):
+                if g_ != r_ and abs(ref_s[g_] - ref_s[r_]) > 1e-3 * abs(ref_s[r_]):
+                    ok = False
+            n_chk += 1
+            if n_chk >= args.check_queries and cpu_s >= args.cpu_seconds:
+                break
+        result["parity"] = {"queries_checked": n_chk, "scores_rtol": 1e-3, "topk_match": ok}
         if world == 1 and not args.no_cpu:
             result["cpu_baseline"] = {"value": cpu_cells / cpu_s, "unit": UNIT, "cores": 1, "kind": "port",
-                                      "sample": f"{n_check} cfg2 queries (oracle/maxsim_ref: float64 GEMM + max + "
-                                                f"fsum + lexsort, OPENBLAS 1 thread), {cpu_s:.1f} s"}
+                                      "sample": f"{n_chk} {cfg.name} queries through oracle/maxsim_ref (float64 GEMM "
+                                                f"+ column max + math.fsum + lexsort, BLAS 1 thread), {cpu_s:.1f} s"}
+        del lim
 
     # ------------------------------------------------ end-to-end through the public host API
     if not args.no_e2e:
@@ -240,11 +274,93 @@ def run_ours(args, rank, world, local_rank):
             e_ms = float(t.item()) / e_steps
             result["e2e"] = {"value": cells_per_step * world / (e_ms / 1e3), "unit": UNIT,
                              "h2d_bytes_per_step": hb.h2d_bytes, "d2h_bytes_per_step": int(nq * K * 8),
-                             "ms_per_step": e_ms}
-            ok = out[0].numpy().tolist() == idx.cpu().numpy().tolist()
-            result["e2e"]["topk_equals_device_path"] = bool(ok)
+                             "ms_per_step": e_ms, "api": "batch.rerank_topk_host (pinned host -> device -> host)",
+                             "topk_equals_device_path": bool(out[0].numpy().tolist() == idx.cpu().numpy().tolist())}
+        del hb
+
+    # ------------------------------------------------ P2: the Col-Bandit loop on the same batch
+    if not args.no_bandit:
+        bandit = run_bandit(args, batch, host_off, cfg, rank, world)
+        if rank == 0:
+            result["bandit"] = bandit
     if rank == 0:
         print(json.dumps(result), flush=True)
+
+
+def run_bandit(args, batch, host_off, cfg, rank, world):
+    import numpy as np
+    import torch
+
+    from paper_2602_02827_b200 import BanditConfig, BanditJob, run_batch
+    from paper_2602_02827_b200.bandit import collect
+
+    qo, do, qd = host_off
+    nq = batch.n_queries
+    jobs = [BanditJob(BanditConfig(k=cfg.k, seed=(0, q)), int(qd[q + 1] - qd[q]), int(qo[q + 1] - qo[q]), q,
+                      int(qd[q]), (-1.0, 1.0)) for q in range(nq)]
+    lens = np.diff(do)
+    elem = batch.d_tokens.element_size()
+    for _ in range(max(1, min(args.warmup, 2))):
+        collect(run_batch(jobs, batch=batch, sync=False), jobs, return_traces=False)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    raw = run_batch(jobs, batch=batch, sync=False)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    res = collect(raw, jobs)
+    if rank != 0:
+        return None
+    reveals = sum(len(r.reveals) for r in res)
+    gather = 0
+    for j, r in zip(jobs, res):
+        if r.reveals:
+            gather += int(lens[np.array([i for i, _, _ in r.reveals]) + j.row_begin].sum()) * batch.dim * elem
+    hbm_peak, _, peak_kind = _peaks()
+    cov = np.array([r.coverage for r in res])
+    out = {"what": "Col-Bandit run() per query (one CTA each), BanditConfig defaults, generic bounds (-1, 1), "
+                   "seed (0, q)",
+           "runs": len(jobs), "ms": ms, "queries_per_s": len(jobs) * world / (ms / 1e3),
+           "revealed_cells_per_s": reveals * world / (ms / 1e3),
+           "iterations": int(sum(r.iterations for r in res)),
+           "coverage_mean": float(cov.mean()), "coverage_min": float(cov.min()), "coverage_max": float(cov.max()),
+           "roofline": {"bound": "hbm (gather)", "achieved": gather / (ms / 1e3) / 1e9, "peak": hbm_peak,
+                        "unit": "GB/s", "frac": gather / (ms / 1e3) / 1e9 / hbm_peak, "peak_kind": peak_kind,
+                        "alg_bytes": gather,
+                        "note": "algorithmic gather = sum over reveals of L_i*d*s (warm-up included); repeated "
+                                "boundary rows hit L2/L1, so this can exceed DRAM traffic"},
+           "gpu_launches": 1}
+    # parity + CPU baseline on sampled queries: the oracle loop must reproduce the device trace
+    from oracle import bandit_ref, maxsim_ref
+
+    lim = _blas_one_thread()
+    n_chk, same, cpu_s, cpu_rev, cov_err = 0, True, 0.0, 0, 0.0
+    for q in range(nq):
+        qt, docs = _query_host(batch, host_off, q)
+        t0 = time.perf_counter()
+        cells = maxsim_ref.cell_matrix(qt, docs)
+        ref = bandit_ref.run(cells, -1.0, 1.0, cfg.k, seed=(0, q))
+        cpu_s += time.perf_counter() - t0
+        cpu_rev += len(ref.reveals)
+        same &= (ref.reveals == res[q].reveals and ref.topk == res[q].topk)
+        cov_err = max(cov_err, abs(ref.coverage - res[q].coverage))
+        n_chk += 1
+        if n_chk >= args.check_queries and cpu_s >= args.cpu_seconds / 2:
+            break
+    del lim
+    out["parity"] = {"queries_checked": n_chk, "trace_identical": bool(same), "coverage_abs_err_max": cov_err}
+    if world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = {"value": cpu_rev / cpu_s, "unit": "revealed cells/s", "cores": 1, "kind": "port",
+                               "queries_per_s": n_chk / cpu_s,
+                               "sample": f"{n_chk} {cfg.name} queries: oracle/maxsim_ref cells + oracle/bandit_ref run, "
+                                         f"{cpu_s:.1f} s"}
+    return out
 
 
 # ---------------------------------------------------------------------------- reference arm
@@ -280,7 +396,7 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     workers = max(1, min(cores, args.ref_workers or cores))
     ctx = mp.get_context("fork")
-    # each worker generates query 0 of the config once (untimed), then scores it once per step
+    # each worker generates one query of the config once (untimed), then scores it once per step
     with cf.ProcessPoolExecutor(workers, mp_context=ctx, initializer=_ref_init, initargs=(cfg.name, 0)) as ex:
         for _ in range(args.warmup):
             list(ex.map(_ref_task, range(workers)))
@@ -296,11 +412,11 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
         "data": "synthetic (numpy, BASELINE.json configs[1] recipe)",
-        "config": {"workload": f"{cfg.name}: {cfg.n_docs} docs/query, Lq={cfg.lq[0]}, d={cfg.dim}, K={cfg.k}",
-                   "queries_per_step": workers},
+        "config": {"workload": f"{cfg.name}: {cfg.n_docs} docs/query, Lq={cfg.lq[0]}, d={cfg.dim}, {cfg.dtype}, "
+                               f"K={cfg.k}", "queries_per_step": workers},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": f"{workers} cfg2 queries per step, one per process (ProcessPoolExecutor, "
-                                   f"OPENBLAS 1 thread each; oracle/maxsim_ref)"},
+                         "sample": f"{workers} {cfg.name} queries per step, one per process (ProcessPoolExecutor, "
+                                   f"BLAS 1 thread each; oracle/maxsim_ref)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -314,9 +430,11 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--queries", type=int, default=None)
     ap.add_argument("--check-queries", type=int, default=4)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-workers", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-bandit", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
