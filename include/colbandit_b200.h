@@ -161,7 +161,8 @@ typedef struct cbx_bandit_run_desc {
   int32_t k;              /* Top-K target, 1..N (k == 0 is answered on the host) */
   int32_t explore_mode;   /* CBX_EPSILON_GREEDY / CBX_STATIC_WARMUP / CBX_UNIFORM_ROW */
   int32_t n_warm;         /* static warm-up cell count                        */
-  int32_t pad0;
+  int32_t flags;          /* bit 0: boundary selection through tournament trees (O(log N) per
+                             reveal) instead of a full pool scan; the host sets it for large pools */
   int64_t warm_off;       /* offset of this run's cells in warm_cells         */
   double alpha_ef;
   double epsilon;
@@ -183,7 +184,9 @@ typedef struct cbx_bandit_out {
   int32_t pad;
 } cbx_bandit_out;
 
-/* Device scratch for `total_rows` rows over all runs of one call. */
+/* Device scratch for `total_rows` rows over all runs of one call; every run's
+ * state_off range must span n_rows + CBX_BANDIT_ROW_SLACK rows. */
+#define CBX_BANDIT_ROW_SLACK 64
 CBX_API size_t cbx_bandit_state_bytes(int64_t total_rows);
 
 /* Run n_runs independent bandits, one CTA each, entirely on the device.

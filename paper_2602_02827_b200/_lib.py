@@ -19,6 +19,8 @@ CBX_F32, CBX_F16, CBX_BF16, CBX_F64 = 0, 1, 2, 3
 CBX_PATH_AUTO, CBX_PATH_TC, CBX_PATH_SIMT = 0, 1, 2
 CBX_EPSILON_GREEDY, CBX_STATIC_WARMUP, CBX_UNIFORM_ROW = 0, 1, 2
 CBX_TERM_SEPARATION, CBX_TERM_EXHAUSTION = 0, 1
+CBX_BANDIT_ROW_SLACK = 64
+CBX_BANDIT_TREE = 1
 
 
 class CbxBatch(ctypes.Structure):
@@ -61,7 +63,7 @@ class CbxBanditRunDesc(ctypes.Structure):
         ("k", ctypes.c_int32),
         ("explore_mode", ctypes.c_int32),
         ("n_warm", ctypes.c_int32),
-        ("pad0", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
         ("warm_off", ctypes.c_int64),
         ("alpha_ef", ctypes.c_double),
         ("epsilon", ctypes.c_double),

@@ -33,6 +33,7 @@ EXPLORE_MODES = ("epsilon-greedy", "static-warmup", "uniform-row")
 _MODE_CODE = {"epsilon-greedy": _lib.CBX_EPSILON_GREEDY, "static-warmup": _lib.CBX_STATIC_WARMUP,
               "uniform-row": _lib.CBX_UNIFORM_ROW}
 MAX_COLS = 64
+TREE_ROWS = 2560  # pools larger than this select boundary rows through tournament trees
 
 
 @dataclass(frozen=True)
@@ -99,6 +100,7 @@ class BanditJob:
     query: int = 0          # token source: query index in the batch
     row_begin: int = 0      # global doc index (token source) / matrix row of row 0
     bounds: CellBounds | tuple[float, float] = (-1.0, 1.0)
+    selection: str = "auto"  # "scan" | "tree" | "auto" (tree for pools above TREE_ROWS)
 
 
 def _rng_state(seed, explore_mode, gamma_init, total_cells):
@@ -162,9 +164,13 @@ def run_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, return_traces:
         d.n_warm, d.warm_off = len(warm), w_off
         warm_parts.append(warm)
         w_off += len(warm)
+        if job.selection not in ("auto", "scan", "tree"):
+            raise ValueError(f"selection must be 'auto', 'scan' or 'tree', got {job.selection!r}")
+        tree = job.selection == "tree" or (job.selection == "auto" and N > TREE_ROWS)
+        d.flags = _lib.CBX_BANDIT_TREE if tree else 0
         d.trace_off, d.state_off = tr_off, st_off
         tr_off += N * T
-        st_off += N
+        st_off += N + _lib.CBX_BANDIT_ROW_SLACK
         max_rows, max_k = max(max_rows, N), max(max_k, cfg.k)
     nl = len(live)
     if nl == 0:

@@ -73,6 +73,10 @@ struct RowsView {
   }
 };
 constexpr size_t ROW_BYTES = 8 * 8 + 4 + 1 + 1;
+// tournament-tree nodes get 4 bytes per row (+ CBX_BANDIT_ROW_SLACK rows of slack per run)
+constexpr size_t ROW_STRIDE = ROW_BYTES + 4;
+constexpr int BD_ROW_SLACK = 64;
+static_assert(BD_ROW_SLACK == CBX_BANDIT_ROW_SLACK, "row slack");
 
 struct BanditParams {
   // token source (nullptr q_tokens -> matrix source)
@@ -189,6 +193,94 @@ __device__ __forceinline__ Cand warp_best(Cand c) {
   return Cand{best, t};
 }
 constexpr uint32_t TIE_EMPTY = 0xFFFFFFFFu;
+
+
+// ----------------------------------------------------------------- tournament trees
+// Four 32-ary trees over the rows, one per selection (i+, i-, best non-member,
+// worst member). Level 0 node g summarises rows [32g, 32g + 32); level l node g
+// summarises level l-1 nodes [32g, 32g + 32); the single top node is the
+// answer. A changed row costs one warp pass per level (32-wide redux), so a
+// reveal is O(log32 N) instead of a scan of the pool.
+struct Trees {
+  uint64_t* key;   // [4][nn]
+  uint32_t* tie;   // [4][nn]
+  int nn, nlev;
+  int off[8], size[8];
+  __device__ void carve(uint8_t* base, int N) {
+    nlev = 0;
+    nn = 0;
+    int sz = (N + 31) / 32;
+    while (true) {
+      off[nlev] = nn;
+      size[nlev] = sz;
+      nn += sz;
+      ++nlev;
+      if (sz == 1 || nlev == 8) break;
+      sz = (sz + 31) / 32;
+    }
+    key = reinterpret_cast<uint64_t*>(base);
+    tie = reinterpret_cast<uint32_t*>(key + 4 * nn);
+  }
+  __device__ __forceinline__ Cand root(int s) const {
+    const int r = s * nn + off[nlev - 1];
+    return Cand{key[r], tie[r]};
+  }
+};
+
+// warp-collective: level-0 node g from its 32 rows
+__device__ __forceinline__ void tree_leaf(const Trees& t, const RowsView& rv, int N, int g, int lane) {
+  const int i = g * 32 + lane;
+  Cand c[4] = {{0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}};
+  if (i < N) {
+    const uint64_t pk = ord_key(rv.proxy[i]);
+    if (rv.member[i]) {
+      c[0] = Cand{~ord_key(rv.lcb[i]), (uint32_t)i};
+      c[3] = Cand{~pk, ~(uint32_t)i};
+    } else {
+      c[1] = Cand{ord_key(rv.ucb[i]), (uint32_t)i};
+      c[2] = Cand{pk, (uint32_t)i};
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const Cand w = warp_best(c[s]);
+    if (lane == 0) {
+      t.key[s * t.nn + g] = w.key;
+      t.tie[s * t.nn + g] = w.tie;
+    }
+  }
+}
+
+// warp-collective: level-l node g from its children at level l-1
+__device__ __forceinline__ void tree_node(const Trees& t, int l, int g, int lane) {
+  const int c0 = g * 32 + lane;
+  const bool ok = c0 < t.size[l - 1];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    Cand c{0, TIE_EMPTY};
+    if (ok) {
+      const int idx = s * t.nn + t.off[l - 1] + c0;
+      c = Cand{t.key[idx], t.tie[idx]};
+    }
+    const Cand w = warp_best(c);
+    if (lane == 0) {
+      t.key[s * t.nn + t.off[l] + g] = w.key;
+      t.tie[s * t.nn + t.off[l] + g] = w.tie;
+    }
+  }
+}
+
+// warp-collective: refresh the path of row i
+__device__ __forceinline__ void tree_update_row(const Trees& t, const RowsView& rv, int N, int i, int lane) {
+  int g = i / 32;
+  tree_leaf(t, rv, N, g, lane);
+  for (int l = 1; l < t.nlev; ++l) {
+    __syncwarp();
+    g /= 32;
+    tree_node(t, l, g, lane);
+  }
+  __syncwarp();
+}
 
 // ----------------------------------------------------------------- row arithmetic
 // refresh(i) of bandit.py:220-247 / compute_decision_state (bounds.py:244-256);
@@ -340,9 +432,12 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
   double* sq_log = reinterpret_cast<double*>(red + 4 * BD_WARPS);     // [BD_MAX_T + 1]
   double* sq_rho = sq_log + BD_MAX_T + 1;                             // [BD_MAX_T + 1]
   uint8_t* row_base = reinterpret_cast<uint8_t*>(sq_rho + BD_MAX_T + 1);
-  if (!P.use_smem) row_base = P.g_rows + (size_t)R.state_off * ROW_BYTES;
+  if (!P.use_smem) row_base = P.g_rows + (size_t)R.state_off * ROW_STRIDE;
   RowsView rv;
   rv.carve(row_base, N);
+  const bool use_tree = (R.flags & 1) != 0;
+  Trees tr;
+  tr.carve(row_base + align_up_dev(ROW_BYTES * (size_t)N, 16), N);
   ExpStore* g_obs = P.g_obs + R.state_off;
   ExpStore* g_lo = P.g_lo + R.state_off;
   ExpStore* g_hi = P.g_hi + R.state_off;
@@ -465,6 +560,15 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       }
       __syncthreads();
     }
+    if (use_tree) {
+      for (int l = 0; l < tr.nlev; ++l) {
+        for (int g = warp; g < tr.size[l]; g += BD_WARPS) {
+          if (l == 0) tree_leaf(tr, rv, N, g, lane);
+          else tree_node(tr, l, g, lane);
+        }
+        __syncthreads();
+      }
+    }
   };
 
   // ------------------------------------------------------------ initial state (all n = 0)
@@ -547,7 +651,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
   while (true) {
     BD_PHASE(3);
     // ---------------------------------------------------------- boundary selection
-    {
+    if (!use_tree) {
       Cand c[4] = {{0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}};
       for (int i = tid; i < N; i += BD_THREADS) {
         const uint64_t pk = ord_key(rv.proxy[i]);
@@ -564,13 +668,19 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
         const Cand w = warp_best(c[s]);
         if (lane == 0) red[s * BD_WARPS + warp] = w;
       }
+      __syncthreads();
     }
-    __syncthreads();
     BD_PHASE(0);
     if (warp == 0) {
       Cand f[4];
+      if (use_tree) {
 #pragma unroll
-      for (int s = 0; s < 4; ++s) f[s] = warp_best(lane < BD_WARPS ? red[s * BD_WARPS + lane] : Cand{0, TIE_EMPTY});
+        for (int s = 0; s < 4; ++s) f[s] = tr.root(s);
+      } else {
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+          f[s] = warp_best(lane < BD_WARPS ? red[s * BD_WARPS + lane] : Cand{0, TIE_EMPTY});
+      }
       if (lane == 0) {
         ctrl->iterations += 1;
         ctrl->swap_in = f[2].key ? (int)f[2].tie : -1;
@@ -705,6 +815,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       __syncthreads();
     }
     BD_PHASE(2);
+    int partner = -1;
     if (tid == 0) {
       const double v = tokens ? ord_val(ctrl->cellkey) : P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
       const int64_t pos = ctrl->n_reveals;
@@ -722,6 +833,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
           if (bk > mk || (bk == mk && b < i_star)) {
             rv.member[i_star] = 0;
             rv.member[b] = 1;
+            partner = b;
           }
         }
       } else {
@@ -731,9 +843,16 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
           if (mk > wk || (mk == wk && i_star < w)) {
             rv.member[i_star] = 1;
             rv.member[w] = 0;
+            partner = w;
           }
         }
       }
+    }
+    if (use_tree && warp == 0) {
+      __syncwarp();
+      partner = __shfl_sync(0xffffffffu, partner, 0);
+      tree_update_row(tr, rv, N, i_star, lane);
+      if (partner >= 0) tree_update_row(tr, rv, N, partner, lane);
     }
     __syncthreads();
   }
@@ -785,7 +904,7 @@ static size_t state_parts(int64_t rows, size_t* off_obs, size_t* off_lo, size_t*
   *off_hi = o;
   o += align_up(sizeof(ExpStore) * (size_t)rows, 256);
   *off_rows = o;
-  o += align_up(ROW_BYTES * (size_t)rows + 64, 256);
+  o += align_up(ROW_STRIDE * (size_t)rows + 64, 256);
   return o;
 }
 
@@ -873,7 +992,7 @@ int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix, 
   size_t smem = 128 + sizeof(Cand) * 4 * BD_WARPS + 2 * sizeof(double) * (BD_MAX_T + 1);
   smem = align_up(smem, 16);
   P.use_smem = max_rows <= BD_SMEM_ROWS ? 1 : 0;
-  if (P.use_smem) smem += (size_t)max_rows * ROW_BYTES + 64;
+  if (P.use_smem) smem += (size_t)(max_rows + BD_ROW_SLACK) * ROW_STRIDE + 64;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int dt = b ? b->dtype : CBX_F64;
   const int dim = b ? b->dim : 16;

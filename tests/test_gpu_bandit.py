@@ -197,3 +197,32 @@ def test_random_matrix_cases_against_oracle():
             assert got.reveals == ref.reveals
             assert got.topk == ref.topk and got.iterations == ref.iterations
             assert got.terminated_by == ref.terminated_by
+
+
+@pytest.mark.parametrize("selection", ["tree", "scan"])
+def test_tree_and_scan_selection_agree_with_the_oracle(selection):
+    """Both boundary-selection structures reproduce the oracle trace (golden matrix cases + a 3000-row pool)."""
+    from paper_2602_02827_b200 import BanditConfig, BanditJob, CellBounds, run_batch
+
+    import torch as _t
+
+    for case in _cases():
+        if case["source"] != "matrix":
+            continue
+        cfg = dict(case["cfg"])
+        cfg["seed"] = _seed(cfg["seed"])
+        m = np.array(case["cells"])
+        job = BanditJob(BanditConfig(**cfg), m.shape[0], m.shape[1], 0, 0,
+                        CellBounds(np.array(case["lo"]), np.array(case["hi"])), selection=selection)
+        res = run_batch([job], matrix=_t.from_numpy(m).cuda())[0]
+        _assert_same(res, case["result"])
+    from helpers import batch_of_cases
+
+    case = W.gen_query("cfg2", 7, n_docs=3000)
+    b = batch_of_cases([case])
+    cells = maxsim_ref.cell_matrix(case.query64(), case.docs64())
+    for k in (1, 10, 100):
+        res = run_batch([BanditJob(BanditConfig(k=k, seed=(0, 7)), 3000, 32, 0, 0, (-1.0, 1.0), selection=selection)],
+                        batch=b)[0]
+        ref = bandit_ref.run(cells, -1.0, 1.0, k, seed=(0, 7))
+        assert res.reveals == ref.reveals and res.topk == ref.topk and res.iterations == ref.iterations

@@ -1,0 +1,100 @@
+"""All five BASELINE configs on one GPU: P1 (scores + Top-K) and P2 (bandit) timings, parity on samples.
+
+Writes one JSON line per config (used for DESIGN.md / profiles tables). Not the driver's bench.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from oracle import bandit_ref, maxsim_ref  # noqa: E402
+from paper_2602_02827_b200 import BanditConfig, BanditJob, run_batch  # noqa: E402
+from paper_2602_02827_b200 import workloads as W  # noqa: E402
+from paper_2602_02827_b200.bandit import collect  # noqa: E402
+from paper_2602_02827_b200.batch import maxsim_scores, topk  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--configs", default="cfg1,cfg2,cfg3,cfg4,cfg5")
+ap.add_argument("--no-bandit", action="store_true")
+ap.add_argument("--check", type=int, default=1)
+a = ap.parse_args()
+peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
+for name in a.configs.split(","):
+    cfg = W.CONFIGS[name]
+    t0 = time.time()
+    b, (qo, do, qd) = W.gen_batch_device(cfg)
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    nq = b.n_queries
+    sc = torch.empty(b.n_docs, dtype=torch.float32, device="cuda")
+    path = "auto"
+    for _ in range(3):
+        maxsim_scores(b, path=path, out=sc)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    for _ in range(5):
+        maxsim_scores(b, path=path, out=sc)
+    e[1].record()
+    idx, _ = topk(sc, b.q_doc_off, cfg.k, b.max_q_docs)
+    e[2].record()
+    torch.cuda.synchronize()
+    ms = e[0].elapsed_time(e[1]) / 5
+    gb = (b.d_tokens.numel() * b.d_tokens.element_size() + b.q_tokens.numel() * b.q_tokens.element_size() + 4 * b.n_docs) / 1e9
+    cells = int((np.diff(qd) * np.diff(qo)).sum())
+    out = {"config": name, "queries": nq, "docs": int(b.n_docs), "doc_tokens": int(b.d_tokens.shape[0]),
+           "p1_ms": ms, "p1_topk_ms": e[1].elapsed_time(e[2]), "p1_gbs": gb / ms * 1e3, "p1_frac": gb / ms * 1e3 / peak,
+           "p1_cells_per_s": cells / ms * 1e3, "p1_queries_per_s": nq / ms * 1e3, "gen_s": gen_s}
+    # parity on the first queries
+    ok = True
+    for q in range(min(a.check, nq)):
+        d0, d1 = int(qd[q]), int(qd[q + 1])
+        qt = b.q_tokens[int(qo[q]):int(qo[q + 1])].double().cpu().numpy()
+        dt = b.d_tokens[int(do[d0]):int(do[d1])].double().cpu().numpy()
+        docs = [dt[int(do[i] - do[d0]):int(do[i + 1] - do[d0])] for i in range(d0, d1)]
+        s, t, cells_m = maxsim_ref.score_query(qt, docs, cfg.k)
+        rt = 1e-5 if cfg.dtype == "f32" else 1e-3
+        ok &= bool(np.allclose(sc.cpu().numpy()[d0:d1], s, rtol=rt))
+        gi = idx[q].cpu().tolist()
+        ok &= all(g == r or abs(s[g] - s[r]) <= rt * abs(s[r]) for g, r in zip(gi, t))
+    out["p1_parity"] = ok
+    if not a.no_bandit:
+        jobs = [BanditJob(BanditConfig(k=cfg.k, alpha_ef=al, seed=(0, q)), int(qd[q + 1] - qd[q]), int(qo[q + 1] - qo[q]),
+                          q, int(qd[q]), (-1.0, 1.0)) for q in range(nq) for al in cfg.alphas]
+        t1 = time.time()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        raw = run_batch(jobs, batch=b, sync=False)
+        e1.record()
+        torch.cuda.synchronize()
+        bms = e0.elapsed_time(e1)
+        res = collect(raw, jobs)
+        lens = np.diff(do)
+        rev = sum(len(r.reveals) for r in res)
+        gather = sum(int(lens[np.array([i for i, _, _ in r.reveals]) + j.row_begin].sum()) for j, r in zip(jobs, res) if r.reveals)
+        gather *= b.dim * b.d_tokens.element_size()
+        cov = [r.coverage for r in res]
+        out.update({"p2_runs": len(jobs), "p2_ms": bms, "p2_revealed_cells_per_s": rev / bms * 1e3,
+                    "p2_gather_gbs": gather / bms / 1e6, "p2_gather_frac": gather / bms / 1e6 / peak,
+                    "p2_coverage_mean": float(np.mean(cov)), "p2_iterations": int(sum(r.iterations for r in res))})
+        if cfg.n_docs <= 5000:
+            same = True
+            for ji in range(min(a.check * len(cfg.alphas), len(jobs))):
+                j = jobs[ji]
+                q = j.query
+                d0, d1 = int(qd[q]), int(qd[q + 1])
+                qt = b.q_tokens[int(qo[q]):int(qo[q + 1])].double().cpu().numpy()
+                dt = b.d_tokens[int(do[d0]):int(do[d1])].double().cpu().numpy()
+                docs = [dt[int(do[i] - do[d0]):int(do[i + 1] - do[d0])] for i in range(d0, d1)]
+                cm = maxsim_ref.cell_matrix(qt, docs)
+                ref = bandit_ref.run(cm, -1.0, 1.0, cfg.k, alpha_ef=j.cfg.alpha_ef, seed=(0, q))
+                same &= ref.reveals == res[ji].reveals and ref.topk == res[ji].topk
+            out["p2_trace_parity"] = same
+    print(json.dumps(out), flush=True)
+    del b
+    torch.cuda.empty_cache()

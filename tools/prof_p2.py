@@ -18,6 +18,7 @@ ap.add_argument("--config", default="cfg2")
 ap.add_argument("--queries", type=int, default=None)
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--phases", action="store_true")
+ap.add_argument("--selection", default="auto")
 a = ap.parse_args()
 cfg = W.CONFIGS[a.config]
 b, (qo, do, qd) = W.gen_batch_device(cfg, n_queries=a.queries)
@@ -26,7 +27,7 @@ jobs = []
 for q in range(nq):
     for alpha in cfg.alphas:
         jobs.append(BanditJob(BanditConfig(k=cfg.k, alpha_ef=alpha, seed=(0, q)), int(qd[q + 1] - qd[q]),
-                              int(qo[q + 1] - qo[q]), q, int(qd[q]), (-1.0, 1.0)))
+                              int(qo[q + 1] - qo[q]), q, int(qd[q]), (-1.0, 1.0), selection=a.selection))
 lens = np.diff(do)
 prof = None
 if a.phases:
