@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcbx.so")
+LIB_PATH = os.environ.get("CBX_LIB") or os.path.join(_HERE, "libcbx.so")  # CBX_LIB: experimental builds
 
 CBX_OK, CBX_EINVAL, CBX_ERANGE, CBX_ECUDA, CBX_EINTERNAL = 0, 1, 2, 3, 4
 CBX_F32, CBX_F16, CBX_BF16, CBX_F64 = 0, 1, 2, 3

@@ -24,6 +24,7 @@
 // Ranking and per-row state live in shared memory when the pool fits,
 // otherwise in global memory.
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace cbx {
 
@@ -104,7 +105,11 @@ struct BanditParams {
   double* trace_v;
   cbx_bandit_out* out;
   unsigned long long* prof;  // optional per-run phase cycle counters (cbx_bandit_set_profile)
+  int ring_slots;            // document-token streaming ring in shared memory
+  int slot_bytes;
+  int ring_off;              // byte offset of the ring in dynamic shared memory
 };
+constexpr int BD_MAX_SLOTS = 8;
 
 // ----------------------------------------------------------------- Python semantics
 __device__ __forceinline__ double pymin(double a, double b) { return b < a ? b : a; }
@@ -227,8 +232,9 @@ struct Trees {
   }
 };
 
-// warp-collective: level-0 node g from its 32 rows
-__device__ __forceinline__ void tree_leaf(const Trees& t, const RowsView& rv, int N, int g, int lane) {
+// warp-collective: level-0 node g from its 32 rows (trees in `mask`: bit s = selection s)
+__device__ __forceinline__ void tree_leaf(const Trees& t, const RowsView& rv, int N, int g, int lane,
+                                          unsigned mask = 0xFu) {
   const int i = g * 32 + lane;
   Cand c[4] = {{0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}};
   if (i < N) {
@@ -243,6 +249,7 @@ __device__ __forceinline__ void tree_leaf(const Trees& t, const RowsView& rv, in
   }
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
+    if (!(mask >> s & 1u)) continue;
     const Cand w = warp_best(c[s]);
     if (lane == 0) {
       t.key[s * t.nn + g] = w.key;
@@ -252,11 +259,12 @@ __device__ __forceinline__ void tree_leaf(const Trees& t, const RowsView& rv, in
 }
 
 // warp-collective: level-l node g from its children at level l-1
-__device__ __forceinline__ void tree_node(const Trees& t, int l, int g, int lane) {
+__device__ __forceinline__ void tree_node(const Trees& t, int l, int g, int lane, unsigned mask = 0xFu) {
   const int c0 = g * 32 + lane;
   const bool ok = c0 < t.size[l - 1];
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
+    if (!(mask >> s & 1u)) continue;
     Cand c{0, TIE_EMPTY};
     if (ok) {
       const int idx = s * t.nn + t.off[l - 1] + c0;
@@ -270,14 +278,15 @@ __device__ __forceinline__ void tree_node(const Trees& t, int l, int g, int lane
   }
 }
 
-// warp-collective: refresh the path of row i
-__device__ __forceinline__ void tree_update_row(const Trees& t, const RowsView& rv, int N, int i, int lane) {
+// warp-collective: refresh the path of row i in the trees of `mask`
+__device__ __forceinline__ void tree_update_row(const Trees& t, const RowsView& rv, int N, int i, int lane,
+                                                unsigned mask) {
   int g = i / 32;
-  tree_leaf(t, rv, N, g, lane);
+  tree_leaf(t, rv, N, g, lane, mask);
   for (int l = 1; l < t.nlev; ++l) {
     __syncwarp();
     g /= 32;
-    tree_node(t, l, g, lane);
+    tree_node(t, l, g, lane, mask);
   }
   __syncwarp();
 }
@@ -405,7 +414,10 @@ template <typename T, int G, int VPL>
 __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParams P) {
   extern __shared__ __align__(16) uint8_t bd_smem[];
   constexpr int NGROUPS = BD_THREADS / G;
-  constexpr int B = VPL == 1 ? 8 : (VPL == 2 ? 4 : 2);
+#ifndef CBX_BD_TOKENS_IN_FLIGHT
+#define CBX_BD_TOKENS_IN_FLIGHT 8
+#endif
+  constexpr int B = VPL == 1 ? CBX_BD_TOKENS_IN_FLIGHT : (VPL == 2 ? CBX_BD_TOKENS_IN_FLIGHT / 2 : CBX_BD_TOKENS_IN_FLIGHT / 4);
   constexpr int GW = G <= 32 ? G : 32;
   const cbx_bandit_run_desc R = P.runs[blockIdx.x];
   const int N = R.n_rows, TC = R.n_cols, K = R.k;
@@ -532,7 +544,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
   // H[i, t] by one warp (warm-up cells)
   auto cell_warp = [&](int i, int t) -> double {
     if (!tokens) return P.matrix[(R.row_begin + i) * P.ld_matrix + t];
-    double best = tokens_max_dot<T, GW, VPL, (VPL == 1 ? 4 : 2)>(dtok, dto[i], dto[i + 1], qtok + (int64_t)t * dim,
+    double best = tokens_max_dot<T, GW, VPL, (VPL == 1 ? 8 : 4)>(dtok, dto[i], dto[i + 1], qtok + (int64_t)t * dim,
                                                                    dim, lane / GW, 32 / GW, lane % GW, init_cell);
 #pragma unroll
     for (int o = 16; o >= GW; o >>= 1) {
@@ -851,8 +863,11 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
     if (use_tree && warp == 0) {
       __syncwarp();
       partner = __shfl_sync(0xffffffffu, partner, 0);
-      tree_update_row(tr, rv, N, i_star, lane);
-      if (partner >= 0) tree_update_row(tr, rv, N, partner, lane);
+      // a member lives in trees 0 (i+) and 3 (worst), a non-member in 1 (i-) and 2 (best non-member);
+      // a membership swap touches all four for both rows
+      const unsigned mask = partner >= 0 ? 0xFu : (rv.member[i_star] ? 0x9u : 0x6u);
+      tree_update_row(tr, rv, N, i_star, lane, mask);
+      if (partner >= 0) tree_update_row(tr, rv, N, partner, lane, 0xFu);
     }
     __syncthreads();
   }
@@ -993,6 +1008,9 @@ int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix, 
   smem = align_up(smem, 16);
   P.use_smem = max_rows <= BD_SMEM_ROWS ? 1 : 0;
   if (P.use_smem) smem += (size_t)(max_rows + BD_ROW_SLACK) * ROW_STRIDE + 64;
+  P.ring_slots = 0;
+  P.slot_bytes = 0;
+  P.ring_off = 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int dt = b ? b->dtype : CBX_F64;
   const int dim = b ? b->dim : 16;
