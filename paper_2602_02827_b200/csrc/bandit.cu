@@ -105,11 +105,7 @@ struct BanditParams {
   double* trace_v;
   cbx_bandit_out* out;
   unsigned long long* prof;  // optional per-run phase cycle counters (cbx_bandit_set_profile)
-  int ring_slots;            // document-token streaming ring in shared memory
-  int slot_bytes;
-  int ring_off;              // byte offset of the ring in dynamic shared memory
 };
-constexpr int BD_MAX_SLOTS = 8;
 
 // ----------------------------------------------------------------- Python semantics
 __device__ __forceinline__ double pymin(double a, double b) { return b < a ? b : a; }
@@ -341,6 +337,42 @@ __device__ __forceinline__ bool to_fixed(double v, long long& q) {
   return true;
 }
 
+// Slow exact-sum paths (rows whose values left the 2^-48 grid, per-cell bounds) are kept out of
+// line so their 8-partial expansions do not inflate the register budget of the hot loop.
+__device__ __noinline__ bool exp_leave_grid(ExpStore* st, long long f, double v) {
+  const double hi = __ll2double_rn(f);
+  const double lo = __ll2double_rn(f - __double2ll_rn(hi));
+  Expansion<BD_CAP> e;
+  e.clear();
+  bool ok = e.add(__dmul_rn(lo, BD_FX_INV));
+  ok &= e.add(__dmul_rn(hi, BD_FX_INV));
+  ok &= e.add(v);
+  store_exp(*st, e);
+  return ok;
+}
+__device__ __noinline__ bool exp_add(ExpStore* st, double v, double* rounded) {
+  Expansion<BD_CAP> e;
+  load_exp(e, *st);
+  const bool ok = e.add(v);
+  store_exp(*st, e);
+  if (rounded) *rounded = e.round();
+  return ok;
+}
+__device__ __noinline__ double exp_value(const ExpStore* st) {
+  Expansion<BD_CAP> e;
+  load_exp(e, *st);
+  return e.round();
+}
+__device__ __noinline__ bool exp_init(ExpStore* st, const double* vals, int n, double* rounded) {
+  Expansion<BD_CAP> e;
+  e.clear();
+  bool ok = true;
+  for (int t = 0; t < n; ++t) ok &= e.add(vals[t]);
+  store_exp(*st, e);
+  *rounded = e.round();
+  return ok;
+}
+
 // ----------------------------------------------------------------- cell source
 // 16-byte vector of token elements -> float64 dot with a float64 slice
 template <typename T>
@@ -469,11 +501,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
 
   // exact sum of a row's revealed values, rounded like math.fsum
   auto obs_sum = [&](int i) -> double {
-    if (rv.exp_mode[i]) {
-      Expansion<BD_CAP> e;
-      load_exp(e, g_obs[i]);
-      return e.round();
-    }
+    if (rv.exp_mode[i]) return exp_value(&g_obs[i]);
     return __dmul_rn(__ll2double_rn(rv.fx[i]), BD_FX_INV);
   };
   // add v to row i's exact sum; false on expansion overflow
@@ -485,23 +513,10 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
         return true;
       }
       // leave the grid: the int64 sum becomes an exact two-term expansion
-      const long long f = rv.fx[i];
-      const double hi = __ll2double_rn(f);
-      const double lo = __ll2double_rn(f - __double2ll_rn(hi));
-      Expansion<BD_CAP> e;
-      e.clear();
-      bool ok = e.add(__dmul_rn(lo, BD_FX_INV));
-      ok &= e.add(__dmul_rn(hi, BD_FX_INV));
-      ok &= e.add(v);
-      store_exp(g_obs[i], e);
       rv.exp_mode[i] = 1;
-      return ok;
+      return exp_leave_grid(&g_obs[i], rv.fx[i], v);
     }
-    Expansion<BD_CAP> e;
-    load_exp(e, g_obs[i]);
-    const bool ok = e.add(v);
-    store_exp(g_obs[i], e);
-    return ok;
+    return exp_add(&g_obs[i], v, nullptr);
   };
 
   // ledger._record (oracle.py:305-314) + refresh(i) (bandit.py:220-247) for one row
@@ -523,15 +538,8 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       lo_sum = (TC - n) ? __dmul_rn((double)(TC - n), R.lo_uniform) : 0.0;
       hi_sum = (TC - n) ? __dmul_rn((double)(TC - n), R.hi_uniform) : 0.0;
     } else {
-      Expansion<BD_CAP> x;
-      load_exp(x, g_lo[i]);
-      ok &= x.add(-lo_b[(int64_t)i * TC + t]);
-      store_exp(g_lo[i], x);
-      lo_sum = x.round();
-      load_exp(x, g_hi[i]);
-      ok &= x.add(-hi_b[(int64_t)i * TC + t]);
-      store_exp(g_hi[i], x);
-      hi_sum = x.round();
+      ok &= exp_add(&g_lo[i], -lo_b[(int64_t)i * TC + t], &lo_sum);
+      ok &= exp_add(&g_hi[i], -hi_b[(int64_t)i * TC + t], &hi_sum);
     }
     double px, l, u;
     row_interval(n, m2, obs, lo_sum, hi_sum, TC, R.alpha_ef, sq_log, sq_rho, px, l, u);
@@ -615,19 +623,9 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       lo_sum = __dmul_rn((double)TC, R.lo_uniform);
       hi_sum = __dmul_rn((double)TC, R.hi_uniform);
     } else {
-      Expansion<BD_CAP> a, b;
-      a.clear();
-      b.clear();
-      bool ok = true;
-      for (int t = 0; t < TC; ++t) {
-        ok &= a.add(lo_b[(int64_t)i * TC + t]);
-        ok &= b.add(hi_b[(int64_t)i * TC + t]);
-      }
+      bool ok = exp_init(&g_lo[i], lo_b + (int64_t)i * TC, TC, &lo_sum);
+      ok &= exp_init(&g_hi[i], hi_b + (int64_t)i * TC, TC, &hi_sum);
       if (!ok) ctrl->status = 2;
-      store_exp(g_lo[i], a);
-      store_exp(g_hi[i], b);
-      lo_sum = a.round();
-      hi_sum = b.round();
     }
     double px, l, u;
     row_interval(0, 0.0, 0.0, lo_sum, hi_sum, TC, R.alpha_ef, sq_log, sq_rho, px, l, u);
@@ -1008,9 +1006,7 @@ int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix, 
   smem = align_up(smem, 16);
   P.use_smem = max_rows <= BD_SMEM_ROWS ? 1 : 0;
   if (P.use_smem) smem += (size_t)(max_rows + BD_ROW_SLACK) * ROW_STRIDE + 64;
-  P.ring_slots = 0;
-  P.slot_bytes = 0;
-  P.ring_off = 0;
+
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int dt = b ? b->dtype : CBX_F64;
   const int dim = b ? b->dim : 16;
