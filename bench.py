@@ -252,30 +252,67 @@ def run_ours(args, rank, world, local_rank):
         del lim
 
     # ------------------------------------------------ end-to-end through the public host API
+    # The reranking service keeps the corpus resident in HBM (Corpus = ColBanditReranker.fit); every
+    # step ships the queries and their candidate id lists host -> device (each query's candidates in a
+    # shuffled order), gathers the candidates, scores, selects Top-K and reads it back (pinned host).
     if not args.no_e2e:
-        hb = HostBatch.from_device_batch(batch)
-        out = (torch.empty((nq, K), dtype=torch.int32).pin_memory(), torch.empty((nq, K)).pin_memory())
+        from paper_2602_02827_b200.batch import Corpus
+
+        corpus = Corpus(batch.d_tokens, do)
+        rng = np.random.default_rng(1234 + rank)
+        cand = np.concatenate([qd[q] + rng.permutation(int(qd[q + 1] - qd[q])) for q in range(nq)]).astype(np.int64)
+        cand_t = torch.from_numpy(cand).pin_memory()
+        q_host = batch.q_tokens.cpu().pin_memory()
         for _ in range(2):
-            rerank_topk_host(hb, K, out=out)
+            corpus.rerank_topk(q_host, qo, cand_t, qd, K)
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
+        e_steps = max(3, args.steps)
+        t0 = time.perf_counter()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e_steps = max(2, min(args.steps, 5))
         e0.record(stream)
         for _ in range(e_steps):
-            rerank_topk_host(hb, K, out=out)
+            oi, ov = corpus.rerank_topk(q_host, qo, cand_t, qd, K)
         e1.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        wall_ms = (time.perf_counter() - t0) * 1e3 / e_steps
+        t = torch.tensor([max(e0.elapsed_time(e1) / e_steps, wall_ms)], dtype=torch.float64, device="cuda")
         if world > 1:
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         if rank == 0:
-            e_ms = float(t.item()) / e_steps
+            e_ms = float(t.item())
+            got_docs = np.take_along_axis(cand.reshape(nq, -1), oi.numpy().astype(np.int64), axis=1) \
+                if np.all(np.diff(qd) == qd[1] - qd[0]) else None
+            ref_docs = idx.cpu().numpy().astype(np.int64) + qd[:-1, None]
             result["e2e"] = {"value": cells_per_step * world / (e_ms / 1e3), "unit": UNIT,
-                             "h2d_bytes_per_step": hb.h2d_bytes, "d2h_bytes_per_step": int(nq * K * 8),
-                             "ms_per_step": e_ms, "api": "batch.rerank_topk_host (pinned host -> device -> host)",
-                             "topk_equals_device_path": bool(out[0].numpy().tolist() == idx.cpu().numpy().tolist())}
+                             "h2d_bytes_per_step": int(q_host.numel() * q_host.element_size() + cand.nbytes
+                                                       + 2 * 8 * (nq + 1)),
+                             "d2h_bytes_per_step": int(nq * K * 8), "ms_per_step": e_ms,
+                             "api": "batch.Corpus.rerank_topk: corpus resident in HBM (fit once, untimed); per step "
+                                    "H2D query tokens + candidate ids, device gather, score, Top-K, D2H Top-K; "
+                                    "max of device-event and host wall time",
+                             "topk_equals_device_path": bool(got_docs is not None and
+                                                             np.array_equal(got_docs, ref_docs))}
+        del corpus
+        # cold variant: every document token crosses PCIe each step (no resident corpus)
+        hb = HostBatch.from_device_batch(batch)
+        out = (torch.empty((nq, K), dtype=torch.int32).pin_memory(), torch.empty((nq, K)).pin_memory())
+        rerank_topk_host(hb, K, out=out)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(2):
+            rerank_topk_host(hb, K, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / 2], dtype=torch.float64, device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        if rank == 0:
+            result["e2e_cold"] = {"value": cells_per_step * world / (float(t.item()) / 1e3), "unit": UNIT,
+                                  "h2d_bytes_per_step": hb.h2d_bytes, "d2h_bytes_per_step": int(nq * K * 8),
+                                  "ms_per_step": float(t.item()),
+                                  "api": "batch.rerank_topk_host: all 11.7 GB of doc tokens H2D every step (PCIe bound)"}
         del hb
 
     # ------------------------------------------------ P2: the Col-Bandit loop on the same batch

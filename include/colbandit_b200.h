@@ -136,6 +136,17 @@ CBX_API int cbx_rerank_topk(const cbx_batch* b, int k, int path, float* scores,
 CBX_API int cbx_maxsim_cells_f64(const cbx_batch* b, double* cells, int64_t ld,
                          double* scores_f64, void* stream);
 
+/* Pack candidates of an HBM-resident corpus (ColBanditReranker.fit,
+ * reranker.py:86-104) into a contiguous CSR batch: out_doc_off[j + 1] =
+ * total tokens of candidates 0..j, out_tokens = their rows in candidate
+ * order. cand_ids index the corpus documents; a bad id sets status[0] |= 1
+ * (checked by the caller after synchronising). out_capacity is in rows. */
+CBX_API int cbx_gather_candidates(const void* corpus_tokens, const int64_t* corpus_doc_off,
+                                  int64_t n_corpus_docs, int dim, int dtype,
+                                  const int64_t* cand_ids, int64_t n_cand, void* out_tokens,
+                                  int64_t out_capacity, int64_t* out_doc_off, int* status,
+                                  void* stream);
+
 /* ---------------------------------------------------------------- P2 */
 /* numpy PCG64 bit-generator state (np.random.default_rng(seed)
  * .bit_generator.state): 128-bit state and increment plus the buffered

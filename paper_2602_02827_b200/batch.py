@@ -289,3 +289,106 @@ def rerank_topk_host(hb: HostBatch, k: int, path: str = "auto", out=None):
     out[0].copy_(idx, non_blocking=True)
     out[1].copy_(val, non_blocking=True)
     return out
+
+
+class Corpus:
+    """An HBM-resident document collection scored against per-call candidate lists.
+
+    The reranking-service form of the reference's ``ColBanditReranker``:
+    ``fit`` stores the corpus once (reranker.py:86-104), every ``rerank``
+    scores one candidate pool per query (reranker.py:115-141). Here the
+    corpus tokens live in HBM; a call ships only query tokens and candidate
+    ids host -> device, packs the candidates with ``cbx_gather_candidates``
+    and runs the exhaustive reranker, returning the per-query Top-K
+    (positions in each query's candidate list) to the host.
+    """
+
+    def __init__(self, doc_tokens, doc_offsets, dtype: str | None = None, clamp_negative: bool = False):
+        torch = _lib.require_cuda()
+        off = np.ascontiguousarray(np.asarray(doc_offsets, dtype=np.int64))
+        if off.ndim != 1 or len(off) < 2 or off[0] != 0 or np.any(np.diff(off) <= 0):
+            raise ValueError("doc_offsets must start at 0 and grow strictly (every document needs a token)")
+        if isinstance(doc_tokens, torch.Tensor) and doc_tokens.is_cuda:
+            self.tokens = doc_tokens.contiguous()
+        else:
+            self.tokens = to_torch_tokens(doc_tokens, dtype).contiguous().cuda()
+        if self.tokens.dim() != 2 or self.tokens.shape[0] != off[-1]:
+            raise ValueError("doc_tokens must be [doc_offsets[-1], dim]")
+        dtype_code(self.tokens.dtype)
+        self.offsets_host = off
+        self.lengths = np.diff(off)
+        self.offsets = torch.from_numpy(off).cuda()
+        self.clamp_negative = bool(clamp_negative)
+        self._ws = {}
+
+    @property
+    def n_docs(self) -> int:
+        return len(self.lengths)
+
+    @property
+    def dim(self) -> int:
+        return int(self.tokens.shape[1])
+
+    def _buf(self, name, numel, dtype, pinned=False):
+        import torch
+
+        t = self._ws.get(name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(max(int(numel), 1), dtype=dtype, pin_memory=pinned) if pinned else \
+                torch.empty(max(int(numel), 1), dtype=dtype, device="cuda")
+            self._ws[name] = t
+        return t[:numel]
+
+    def rerank_topk(self, q_tokens, q_tok_off, cand_ids, q_cand_off, k: int, path: str = "auto", sync: bool = True):
+        """Host in, host out: per-query Top-K positions into the candidate list and their scores.
+
+        ``q_tokens`` [sum Lq, dim] (pinned CPU tensor in the corpus dtype), ``q_tok_off`` [nq + 1],
+        ``cand_ids`` [sum N_q] corpus document ids, ``q_cand_off`` [nq + 1] (int64 numpy or CPU tensors).
+        """
+        import torch
+
+        lib = _lib.load()
+        qo = np.asarray(q_tok_off, dtype=np.int64)
+        co = np.asarray(q_cand_off, dtype=np.int64)
+        cid = cand_ids if isinstance(cand_ids, torch.Tensor) else torch.from_numpy(np.asarray(cand_ids, np.int64))
+        nq = len(qo) - 1
+        n_cand = int(co[-1])
+        if cid.numel() != n_cand:
+            raise ValueError("cand_ids length does not match q_cand_off[-1]")
+        cid_np = cid.numpy()
+        if n_cand and (cid_np.min() < 0 or cid_np.max() >= self.n_docs):
+            raise IndexError(f"candidate id out of range [0, {self.n_docs})")
+        total_rows = int(self.lengths[cid_np].sum()) if n_cand else 0
+        # host -> device: the call's inputs only
+        dq = self._buf("q", q_tokens.numel(), q_tokens.dtype).view(q_tokens.shape)
+        dq.copy_(q_tokens, non_blocking=True)
+        hoff = self._buf("hoff", 2 * (nq + 1), torch.int64, pinned=True)
+        hoff[: nq + 1].copy_(torch.from_numpy(qo))
+        hoff[nq + 1:].copy_(torch.from_numpy(co))
+        doffs = self._buf("offs", 2 * (nq + 1), torch.int64)
+        doffs.copy_(hoff, non_blocking=True)
+        dqo, dco = doffs[: nq + 1], doffs[nq + 1:]
+        dcid = self._buf("cid", n_cand, torch.int64)
+        dcid.copy_(cid, non_blocking=True)
+        # pack candidates on the device
+        rows = self._buf("rows", total_rows * self.dim, self.tokens.dtype).view(total_rows, self.dim)
+        doff = self._buf("doff", n_cand + 1, torch.int64)
+        status = self._buf("status", 1, torch.int32)
+        status.zero_()
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(lib.cbx_gather_candidates(self.tokens.data_ptr(), self.offsets.data_ptr(), self.n_docs, self.dim,
+                                             dtype_code(self.tokens.dtype), dcid.data_ptr(), n_cand, rows.data_ptr(),
+                                             total_rows, doff.data_ptr(), status.data_ptr(), stream), "gather")
+        nd = np.diff(co)
+        b = TokenBatch(dq, dqo, rows, doff, dco, self.clamp_negative, int(np.diff(qo).max()) if nq else 0,
+                       int(nd.max()) if nq else 0, total_rows)
+        idx, val, _ = rerank_topk(b, k, path)
+        out_i = self._buf("oi", idx.numel(), torch.int32, pinned=True).view(idx.shape)
+        out_v = self._buf("ov", val.numel(), torch.float32, pinned=True).view(val.shape)
+        out_i.copy_(idx, non_blocking=True)
+        out_v.copy_(val, non_blocking=True)
+        if sync:
+            torch.cuda.current_stream().synchronize()
+            if int(status.item()):
+                raise IndexError("candidate id out of range")
+        return out_i, out_v

@@ -182,3 +182,33 @@ def test_invalid_arguments_raise_value_error():
         rerank_topk(b, 4)
     with pytest.raises(ValueError):
         rerank_topk(b, 2, path="bogus")
+
+
+def test_resident_corpus_rerank_matches_oracle():
+    """Corpus (HBM-resident, fit once) + per-call candidate ids: gather kernel + scorer + Top-K."""
+    from paper_2602_02827_b200.batch import Corpus
+
+    rng = np.random.default_rng(21)
+    d = 128
+    lens = rng.integers(1, 400, size=500)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    toks = W._cast(W._unit(rng.standard_normal((int(off[-1]), d))), "f16")
+    corpus = Corpus(toks, off)
+    queries, cands = [], []
+    for q in range(7):
+        lq = int(rng.integers(1, 40))
+        queries.append(W._cast(W._unit(rng.standard_normal((lq, d))), "f16"))
+        n = int(rng.integers(5, 120))
+        cands.append(rng.choice(500, size=n, replace=q % 2 == 0))  # duplicates allowed
+    qo = np.concatenate([[0], np.cumsum([x.shape[0] for x in queries])]).astype(np.int64)
+    co = np.concatenate([[0], np.cumsum([len(c) for c in cands])]).astype(np.int64)
+    qt = torch.from_numpy(np.concatenate(queries)).pin_memory()
+    k = 5
+    idx, val = corpus.rerank_topk(qt, qo, np.concatenate(cands), co, k)
+    docs64 = [W.to_float64(toks[off[i]:off[i + 1]], "f16") for i in range(500)]
+    for q in range(7):
+        s, t, _ = maxsim_ref.score_query(W.to_float64(queries[q], "f16"), [docs64[c] for c in cands[q]], k)
+        assert topk_matches(idx[q].tolist(), t, s, 1e-3)
+        np.testing.assert_allclose(val[q].numpy(), s[idx[q].numpy()], rtol=1e-3)
+    with pytest.raises(IndexError):
+        corpus.rerank_topk(qt, qo, np.full(int(co[-1]), 500), co, k)
