@@ -147,6 +147,18 @@ CBX_API int cbx_gather_candidates(const void* corpus_tokens, const int64_t* corp
                                   int64_t out_capacity, int64_t* out_doc_off, int* status,
                                   void* stream);
 
+/* Score candidates of an HBM-resident corpus in place (no candidate copy):
+ * the batch's d_tokens / n_d_tokens are the CORPUS token rows, its
+ * q_doc_off ranges index cand_ids (corpus document ids, corpus_off = corpus
+ * CSR offsets). Documents are streamed by TMA straight from the corpus,
+ * packed at 8-row granularity. scores / topk as cbx_rerank_topk; a bad id
+ * sets status[0] |= 1. */
+CBX_API size_t cbx_corpus_workspace_bytes(int64_t n_queries, int64_t n_cand, int64_t max_q_cands, int k);
+CBX_API int cbx_corpus_rerank_topk(const cbx_batch* b, const int64_t* corpus_off, int64_t n_corpus,
+                                   const int64_t* cand_ids, int k, float* scores, int32_t* topk_idx,
+                                   float* topk_val, int* status, void* workspace, size_t ws_bytes,
+                                   void* stream);
+
 /* ---------------------------------------------------------------- P2 */
 /* numpy PCG64 bit-generator state (np.random.default_rng(seed)
  * .bit_generator.state): 128-bit state and increment plus the buffered

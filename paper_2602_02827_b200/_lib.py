@@ -103,6 +103,8 @@ SIGNATURES = {
     "cbx_topk_f64": (_I, [_P, _P, _I64, _I64, _I, _P, _P, _P, _SZ, _P]),
     "cbx_rerank_topk": (_I, [_P, _I, _I, _P, _P, _P, _P, _SZ, _P]),
     "cbx_maxsim_cells_f64": (_I, [_P, _P, _I64, _P, _P]),
+    "cbx_corpus_workspace_bytes": (_SZ, [_I64, _I64, _I64, _I]),
+    "cbx_corpus_rerank_topk": (_I, [_P, _P, _I64, _P, _I, _P, _P, _P, _P, _P, _SZ, _P]),
     "cbx_gather_candidates": (_I, [_P, _P, _I64, _I, _I, _P, _I64, _P, _I64, _P, _P, _P]),
     "cbx_bandit_state_bytes": (_SZ, [_I64]),
     "cbx_bandit_set_profile": (None, [_P]),

@@ -339,11 +339,14 @@ class Corpus:
             self._ws[name] = t
         return t[:numel]
 
-    def rerank_topk(self, q_tokens, q_tok_off, cand_ids, q_cand_off, k: int, path: str = "auto", sync: bool = True):
+    def rerank_topk(self, q_tokens, q_tok_off, cand_ids, q_cand_off, k: int, path: str = "auto", sync: bool = True,
+                    mode: str = "packed"):
         """Host in, host out: per-query Top-K positions into the candidate list and their scores.
 
         ``q_tokens`` [sum Lq, dim] (pinned CPU tensor in the corpus dtype), ``q_tok_off`` [nq + 1],
         ``cand_ids`` [sum N_q] corpus document ids, ``q_cand_off`` [nq + 1] (int64 numpy or CPU tensors).
+        ``mode="packed"`` streams the candidates straight from the corpus (tcgen05 path, no copy);
+        ``mode="gather"`` first packs them into a contiguous batch (any dtype / path).
         """
         import torch
 
@@ -358,7 +361,8 @@ class Corpus:
         cid_np = cid.numpy()
         if n_cand and (cid_np.min() < 0 or cid_np.max() >= self.n_docs):
             raise IndexError(f"candidate id out of range [0, {self.n_docs})")
-        total_rows = int(self.lengths[cid_np].sum()) if n_cand else 0
+        if mode not in ("packed", "gather"):
+            raise ValueError(f"mode must be 'packed' or 'gather', got {mode!r}")
         # host -> device: the call's inputs only
         dq = self._buf("q", q_tokens.numel(), q_tokens.dtype).view(q_tokens.shape)
         dq.copy_(q_tokens, non_blocking=True)
@@ -370,19 +374,38 @@ class Corpus:
         dqo, dco = doffs[: nq + 1], doffs[nq + 1:]
         dcid = self._buf("cid", n_cand, torch.int64)
         dcid.copy_(cid, non_blocking=True)
-        # pack candidates on the device
-        rows = self._buf("rows", total_rows * self.dim, self.tokens.dtype).view(total_rows, self.dim)
-        doff = self._buf("doff", n_cand + 1, torch.int64)
         status = self._buf("status", 1, torch.int32)
         status.zero_()
         stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-        _lib.check(lib.cbx_gather_candidates(self.tokens.data_ptr(), self.offsets.data_ptr(), self.n_docs, self.dim,
-                                             dtype_code(self.tokens.dtype), dcid.data_ptr(), n_cand, rows.data_ptr(),
-                                             total_rows, doff.data_ptr(), status.data_ptr(), stream), "gather")
         nd = np.diff(co)
-        b = TokenBatch(dq, dqo, rows, doff, dco, self.clamp_negative, int(np.diff(qo).max()) if nq else 0,
-                       int(nd.max()) if nq else 0, total_rows)
-        idx, val, _ = rerank_topk(b, k, path)
+        max_lq = int(np.diff(qo).max()) if nq else 0
+        max_nc = int(nd.max()) if nq else 0
+        if mode == "packed":
+            s_ = _lib.CbxBatch()
+            s_.q_tokens, s_.q_tok_off = dq.data_ptr(), dqo.data_ptr()
+            s_.d_tokens, s_.d_tok_off, s_.q_doc_off = self.tokens.data_ptr(), self.offsets.data_ptr(), dco.data_ptr()
+            s_.n_queries, s_.n_docs = nq, n_cand
+            s_.n_q_tokens, s_.n_d_tokens = int(dq.shape[0]), int(self.tokens.shape[0])
+            s_.dim, s_.dtype = self.dim, dtype_code(self.tokens.dtype)
+            s_.clamp_negative, s_.max_lq, s_.max_q_docs, s_.max_q_doc_tokens = int(self.clamp_negative), max_lq, max_nc, 0
+            ws = self._buf("ws", lib.cbx_corpus_workspace_bytes(nq, n_cand, max_nc, k), torch.uint8)
+            scores = self._buf("scores", n_cand, torch.float32)
+            idx = self._buf("idx", nq * k, torch.int32).view(nq, k)
+            val = self._buf("val", nq * k, torch.float32).view(nq, k)
+            _lib.check(lib.cbx_corpus_rerank_topk(ctypes.byref(s_), self.offsets.data_ptr(), self.n_docs,
+                                                  dcid.data_ptr(), k, scores.data_ptr(), idx.data_ptr(),
+                                                  val.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                  stream), "corpus_rerank_topk")
+        else:
+            total_rows = int(self.lengths[cid_np].sum()) if n_cand else 0
+            rows = self._buf("rows", total_rows * self.dim, self.tokens.dtype).view(total_rows, self.dim)
+            doff = self._buf("doff", n_cand + 1, torch.int64)
+            _lib.check(lib.cbx_gather_candidates(self.tokens.data_ptr(), self.offsets.data_ptr(), self.n_docs,
+                                                 self.dim, dtype_code(self.tokens.dtype), dcid.data_ptr(), n_cand,
+                                                 rows.data_ptr(), total_rows, doff.data_ptr(), status.data_ptr(),
+                                                 stream), "gather")
+            b = TokenBatch(dq, dqo, rows, doff, dco, self.clamp_negative, max_lq, max_nc, total_rows)
+            idx, val, _ = rerank_topk(b, k, path)
         out_i = self._buf("oi", idx.numel(), torch.int32, pinned=True).view(idx.shape)
         out_v = self._buf("ov", val.numel(), torch.float32, pinned=True).view(val.shape)
         out_i.copy_(idx, non_blocking=True)

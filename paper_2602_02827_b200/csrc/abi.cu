@@ -32,6 +32,9 @@ int sm_count() {
 // defined in the kernel translation units
 bool tc_supported(const cbx_batch* b);
 int launch_maxsim_tc(const cbx_batch* b, float* scores, cudaStream_t stream);
+int launch_maxsim_tc_packed(const cbx_batch* b, const int64_t* corpus_off, int64_t n_corpus, const int64_t* cand_ids,
+                            float* scores, void* ws, size_t ws_bytes, int* status, cudaStream_t stream);
+size_t packed_plan_bytes(int64_t n_cand);
 int launch_maxsim_exact(const cbx_batch* b, double* cells, int64_t ld, double* s64, float* s32, cudaStream_t st);
 size_t topk_workspace_bytes(int64_t n_queries, int64_t max_q_docs, int K);
 int launch_topk_f32(const float* s, const int64_t* off, int64_t nq, int64_t mx, int K, int32_t* ti, float* tv,
@@ -108,6 +111,28 @@ int cbx_rerank_topk(const cbx_batch* b, int k, int path, float* scores, int32_t*
   int rc = cbx_maxsim_scores(b, scores, path, ws, ws_bytes, stream);
   if (rc) return rc;
   return cbx_topk_f32(scores, b->q_doc_off, b->n_queries, b->max_q_docs, k, topk_idx, topk_val, ws, ws_bytes, stream);
+}
+
+size_t cbx_corpus_workspace_bytes(int64_t n_queries, int64_t n_cand, int64_t max_q_cands, int k) {
+  return align_up(packed_plan_bytes(n_cand), 256) + topk_workspace_bytes(n_queries, max_q_cands, k);
+}
+
+int cbx_corpus_rerank_topk(const cbx_batch* b, const int64_t* corpus_off, int64_t n_corpus, const int64_t* cand_ids,
+                           int k, float* scores, int32_t* topk_idx, float* topk_val, int* status, void* ws,
+                           size_t ws_bytes, void* stream) {
+  int rc = check_batch(b);
+  if (rc) return rc;
+  if (!corpus_off || (b->n_docs && !cand_ids) || !status || !scores) return fail(CBX_EINVAL, "corpus rerank: NULL buffer");
+  if (!tc_supported(b))
+    return fail(CBX_EINVAL, "corpus rerank needs the tcgen05 path (f16/bf16, Lq <= 128, dim % 8 == 0)");
+  if (ws_bytes < cbx_corpus_workspace_bytes(b->n_queries, b->n_docs, b->max_q_docs, k))
+    return fail(CBX_EINVAL, "corpus rerank: workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t plan = align_up(packed_plan_bytes(b->n_docs), 256);
+  rc = launch_maxsim_tc_packed(b, corpus_off, n_corpus, cand_ids, scores, ws, plan, status, st);
+  if (rc) return rc;
+  return cbx_topk_f32(scores, b->q_doc_off, b->n_queries, b->max_q_docs, k, topk_idx, topk_val,
+                      static_cast<uint8_t*>(ws) + plan, ws_bytes - plan, stream);
 }
 
 int cbx_maxsim_cells_f64(const cbx_batch* b, double* cells, int64_t ld, double* scores_f64, void* stream) {

@@ -38,9 +38,15 @@ constexpr int TC_MAX_STAGES = 8;
 
 struct TcParams {
   const int64_t* q_tok_off;
-  const int64_t* d_tok_off;
+  const int64_t* d_tok_off;   // token offsets; in packed mode the 8-aligned packed starts
   const int64_t* q_doc_off;
   float* scores;
+  // packed mode: document j is rows [src_row[j], src_row[j] + doc_len[j]) of a corpus tensor and is
+  // laid out in the tile stream at packed rows [d_tok_off[j], d_tok_off[j] + doc_len[j]), 8-row aligned
+  int32_t packed;
+  const int64_t* src_row;
+  const int32_t* doc_len;
+  const int64_t* n_tokens_dev;  // packed mode: total packed rows (d_tok_off[n_docs]) read on the device
   int64_t n_queries;
   int64_t n_docs;
   int64_t n_tokens;      // total document tokens (partitioned evenly over the CTAs)
@@ -81,7 +87,8 @@ __device__ __forceinline__ int64_t lower_bound_start(const int64_t* __restrict__
 // sequence, so no scheduling state is exchanged.
 struct ChunkCursor {
   int64_t doc, doc_hi, q;
-  __device__ __forceinline__ void init(const TcParams& p) {
+  __device__ __forceinline__ void init(TcParams& p) {
+    if (p.packed) p.n_tokens = *p.n_tokens_dev;
     const int64_t G = gridDim.x, b = blockIdx.x;
     const int64_t x0 = (int64_t)((__int128)p.n_tokens * b / G);
     const int64_t x1 = (int64_t)((__int128)p.n_tokens * (b + 1) / G);
@@ -144,9 +151,15 @@ __device__ __forceinline__ float masked_max(const float (&v)[32], int s, int e, 
   return m;
 }
 
+// tensor maps: doc tiles of box heights tile_n >> k (k = 0..4; packed mode uses all of them to lay
+// documents out at 8-row granularity) and the query rows
+struct TmapSet {
+  CUtensorMap d[5];
+  CUtensorMap q;
+};
+
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    maxsim_tc_kernel(const __grid_constant__ CUtensorMap tmap_d, const __grid_constant__ CUtensorMap tmap_q,
-                     const TcParams p) {
+    maxsim_tc_kernel(const __grid_constant__ TmapSet tm, TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* q_slot = smem;                                    // kblocks x (128 rows x 128 B)
@@ -182,8 +195,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     ptx::fence_mbarrier_init();
   }
   if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tmap_d);
-    ptx::prefetch_tmap(&tmap_q);
+    ptx::prefetch_tmap(&tm.d[0]);
+    ptx::prefetch_tmap(&tm.q);
   }
   if (warp == 1) ptx::tmem_alloc<TC_ACC_BUFS * TC_MAX_TILE_N>(tmem_holder);
   ptx::tc_fence_before();
@@ -192,30 +205,85 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0, qphase = 0;
-      const uint64_t pol = ptx::policy_evict_first();
-      ChunkCursor cur;
-      cur.init(p);
-      ChunkInfo c;
-      while (cur.next(p, c)) {
+    // ------------------------------------------------------------ TMA producer (lane 0 issues)
+    uint32_t stage = 0, phase = 0, qphase = 0;
+    const uint64_t pol = ptx::policy_evict_first();
+    ChunkCursor cur;
+    cur.init(p);
+    ChunkInfo c;
+    while (cur.next(p, c)) {
+      if (lane == 0) {
         // one query slot: reload only after every MMA of the previous chunk retired
         ptx::mbar_wait(qempty, qphase ^ 1);
         ptx::mbar_arrive_expect_tx(qfull, (uint32_t)(p.rep * p.kblocks * p.lqp * 128));
         for (int g = 0; g < p.rep; ++g)
           for (int kb = 0; kb < p.kblocks; ++kb)
-            ptx::tma_load_2d(q_slot + kb * 16384 + g * p.lqp * 128, &tmap_q, qfull, kb * 64, (int32_t)c.q_tok0);
-        qphase ^= 1;
-        for (int t = 0; t < c.ntiles; ++t) {
+            ptx::tma_load_2d(q_slot + kb * 16384 + g * p.lqp * 128, &tm.q, qfull, kb * 64, (int32_t)c.q_tok0);
+      }
+      qphase ^= 1;
+      // packed mode: metadata of 32 documents per lane window (packed start, corpus row, length)
+      int64_t jd = c.doc0, win = c.doc0;
+      int64_t w_pk = 0, w_src = 0;
+      int32_t w_len = 0;
+      if (p.packed && win + lane < c.doc1) {
+        w_pk = __ldg(p.d_tok_off + win + lane);
+        w_src = __ldg(p.src_row + win + lane);
+        w_len = __ldg(p.doc_len + win + lane);
+      }
+      for (int t = 0; t < c.ntiles; ++t) {
+        const int64_t r0 = c.cs + (int64_t)t * p.tile_n;
+        const int64_t r1 = c.ce - r0 < p.tile_n ? c.ce : r0 + p.tile_n;
+        if (lane == 0) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[stage], p.stage_bytes);
-          const int32_t row = (int32_t)(c.cs + (int64_t)t * p.tile_n);
-          uint8_t* dst = stages + (size_t)stage * p.stage_bytes;
-          for (int kb = 0; kb < p.kblocks; ++kb)
-            ptx::tma_load_2d_hint(dst + kb * p.tile_n * 128, &tmap_d, &full[stage], kb * 64, row, pol);
-          if (++stage == (uint32_t)p.stages) { stage = 0; phase ^= 1; }
+          ptx::mbar_arrive_expect_tx(&full[stage], p.packed ? (uint32_t)((r1 - r0) * 128 * p.kblocks) : p.stage_bytes);
         }
+        __syncwarp();
+        uint8_t* dst = stages + (size_t)stage * p.stage_bytes;
+        if (!p.packed) {
+          if (lane == 0)
+            for (int kb = 0; kb < p.kblocks; ++kb)
+              ptx::tma_load_2d_hint(dst + kb * p.tile_n * 128, &tm.d[0], &full[stage], kb * 64, (int32_t)r0, pol);
+        } else {
+          // every document overlapping packed rows [r0, r1): boxes of 8 * 2^k rows at 8-aligned smem rows
+          while (true) {
+            if (jd - win >= 32) {
+              win += 32;
+              w_pk = w_src = 0;
+              w_len = 0;
+              if (win + lane < c.doc1) {
+                w_pk = __ldg(p.d_tok_off + win + lane);
+                w_src = __ldg(p.src_row + win + lane);
+                w_len = __ldg(p.doc_len + win + lane);
+              }
+            }
+            if (jd >= c.doc1) break;
+            const int sl = (int)(jd - win);
+            const int64_t pk = __shfl_sync(0xffffffffu, w_pk, sl);
+            if (pk >= r1) break;
+            const int64_t src = __shfl_sync(0xffffffffu, w_src, sl);
+            const int32_t len = __shfl_sync(0xffffffffu, w_len, sl);
+            const int64_t pk_next = pk + ((len + 7) & ~7);
+            const int64_t ov0 = pk > r0 ? pk : r0;
+            const int64_t ov1 = pk_next < r1 ? pk_next : r1;
+            if (lane == 0) {
+              int64_t row = ov0, srow = src + (ov0 - pk);
+              for (int k = 0; k < 5; ++k) {
+                const int h = p.tile_n >> k;
+                if (h < 8) break;
+                while (ov1 - row >= h) {
+                  for (int kb = 0; kb < p.kblocks; ++kb)
+                    ptx::tma_load_2d_hint(dst + kb * p.tile_n * 128 + (row - r0) * 128, &tm.d[k], &full[stage],
+                                          kb * 64, (int32_t)srow, pol);
+                  row += h;
+                  srow += h;
+                }
+              }
+            }
+            if (pk_next > r1) break;  // document continues into the next tile
+            ++jd;
+          }
+        }
+        if (++stage == (uint32_t)p.stages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -272,10 +340,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       ChunkInfo c;
       while (cursor.next(p, c)) {
         const bool lane_valid = wig * 32 + lane < c.lq;
-        // window of document end offsets: ends[lane] = end of doc (win + lane)
+        // window of document end offsets: ends[lane] = end of doc (win + lane); in packed mode the end
+        // of the valid rows, the next document starting at the following multiple of 8
+        const int64_t align = p.packed ? 7 : 0;
+        auto end_of = [&](int64_t d) -> int64_t {
+          if (d >= c.doc1) return INT64_MAX;
+          return p.packed ? __ldg(p.d_tok_off + d) + __ldg(p.doc_len + d) : __ldg(p.d_tok_off + d + 1);
+        };
         int64_t win = c.doc0;
-        int64_t ends = (win + lane < c.doc1) ? __ldg(p.d_tok_off + win + 1 + lane) : INT64_MAX;
-        int64_t ends_nx = (win + 32 + lane < c.doc1) ? __ldg(p.d_tok_off + win + 33 + lane) : INT64_MAX;
+        int64_t ends = end_of(win + lane);
+        int64_t ends_nx = end_of(win + 32 + lane);
         int64_t doc = c.doc0;
         int64_t prev_end = c.cs;
         for (int t = 0; t < c.ntiles; ++t, ++tg) {
@@ -301,7 +375,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (doc - win >= 32) {
               win += 32;
               ends = ends_nx;
-              ends_nx = (win + 32 + lane < c.doc1) ? __ldg(p.d_tok_off + win + 33 + lane) : INT64_MAX;
+              ends_nx = end_of(win + 32 + lane);
               continue;
             }
             cur_end = __shfl_sync(0xffffffffu, ends, (int)(doc - win));
@@ -309,7 +383,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             prev_end = cur_end;
             ++doc;
           }
-          const bool head_before = prev_end < tb;
+          int64_t doc_start = (prev_end + align) & ~align;
+          const bool head_before = doc_start < tb;
           const int64_t head_doc = doc;
           int nfin = 0;
           float* mypart = part + (pb * 4 + quad) * TC_MAX_TILE_N;
@@ -328,7 +403,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           };
           float cur = init, H = init;
           bool head_open = true;
-          int end_rel = (int)(cur_end - tb < 1 << 20 ? cur_end - tb : 1 << 20);
           auto close_seg = [&]() {
             if (head_open) {
               H = cur;
@@ -338,34 +412,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             cur = init;
             prev_end = cur_end;
+            doc_start = (prev_end + align) & ~align;
             ++doc;
             if (doc - win >= 32) {
               win += 32;
               ends = ends_nx;
-              ends_nx = (win + 32 + lane < c.doc1) ? __ldg(p.d_tok_off + win + 33 + lane) : INT64_MAX;
+              ends_nx = end_of(win + 32 + lane);
             }
             cur_end = __shfl_sync(0xffffffffu, ends, (int)(doc - win));
-            end_rel = (int)(cur_end - tb < 1 << 20 ? cur_end - tb : 1 << 20);
           };
 #pragma unroll
           for (int b = 0; b < TC_MAX_TILE_N / 32; ++b) {
             if (b * 32 >= ncols) break;
-            const int g0 = b * 32;
-            const int nc = ncols - g0 < 32 ? ncols - g0 : 32;
-            if (end_rel >= g0 + nc) {
-              // no document boundary strictly inside this block
-              cur = fmaxf(cur, nc == 32 ? max32(v[b]) : masked_max(v[b], 0, nc, init));
-              if (end_rel == g0 + nc) close_seg();
-            } else {
-              int s = 0;
-              while (true) {
-                const int e = end_rel - g0 < nc ? end_rel - g0 : nc;
-                cur = masked_max(v[b], s, e, cur);
-                if (end_rel - g0 > nc) break;
-                close_seg();
-                s = e;
-                if (s >= nc) break;
-              }
+            const int64_t g0 = tb + b * 32;  // stream row of this block's column 0
+            const int nc = ncols - b * 32 < 32 ? ncols - b * 32 : 32;
+            while (true) {
+              const int64_t ds = doc_start - g0;
+              if (ds >= nc) break;  // the current document starts after this block (packed padding)
+              const int64_t de = cur_end - g0;
+              const int s = ds > 0 ? (int)ds : 0;
+              const int e = de < nc ? (int)de : nc;
+              if (s == 0 && e == 32) cur = fmaxf(cur, max32(v[b]));
+              else cur = masked_max(v[b], s, e, cur);
+              if (de > nc) break;  // document continues past this block
+              close_seg();
             }
           }
           // carry chain: merge the previous tile's open document into this head
@@ -447,9 +517,115 @@ bool tc_supported(const cbx_batch* b) {
          b->dim <= 512 && b->n_d_tokens < (int64_t(1) << 31) && b->n_q_tokens < (int64_t(1) << 31);
 }
 
-int launch_maxsim_tc(const cbx_batch* b, float* scores, cudaStream_t stream) {
-  if (!tc_supported(b)) return fail(CBX_EINVAL, "tcgen05 scorer needs f16/bf16 tokens, Lq <= 128, dim % 8 == 0");
-  if (b->n_docs == 0 || b->n_queries == 0) return CBX_OK;
+// Packed-mode plan: for candidate j (corpus document cand[j]): src_row[j], doc_len[j] and the packed
+// start pk[j] = sum_{i<j} ceil8(len_i) (pk[n] = total). Three-kernel scan (block sums, their scan, add).
+constexpr int PL_THREADS = 512;
+constexpr int PL_PER = 8;
+constexpr int PL_CHUNK = PL_THREADS * PL_PER;
+
+__device__ __forceinline__ int64_t block_excl_scan(int64_t x, int64_t* wsum, int64_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < PL_THREADS / 32 ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < PL_THREADS / 32) wsum[lane] = w;
+  }
+  __syncthreads();
+  total = wsum[PL_THREADS / 32 - 1];
+  const int64_t r = inc - x + (warp ? wsum[warp - 1] : 0);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(PL_THREADS)
+    plan_local_kernel(const int64_t* __restrict__ corpus_off, int64_t n_corpus, const int64_t* __restrict__ cand,
+                      int64_t n, int64_t* __restrict__ pk, int64_t* __restrict__ src_row, int32_t* __restrict__ len,
+                      int64_t* __restrict__ block_tot, int* __restrict__ status) {
+  __shared__ int64_t wsum[PL_THREADS / 32];
+  const int64_t j0 = (int64_t)blockIdx.x * PL_CHUNK + (int64_t)threadIdx.x * PL_PER;
+  int64_t l8[PL_PER], t = 0;
+#pragma unroll
+  for (int u = 0; u < PL_PER; ++u) {
+    l8[u] = 0;
+    const int64_t j = j0 + u;
+    if (j < n) {
+      const int64_t id = cand[j];
+      int64_t L = 0, s0 = 0;
+      if (id < 0 || id >= n_corpus) atomicOr(status, 1);
+      else {
+        s0 = corpus_off[id];
+        L = corpus_off[id + 1] - s0;
+      }
+      src_row[j] = s0;
+      len[j] = (int32_t)L;
+      l8[u] = (L + 7) & ~int64_t(7);
+    }
+    t += l8[u];
+  }
+  int64_t tot;
+  int64_t run = block_excl_scan(t, wsum, tot);
+#pragma unroll
+  for (int u = 0; u < PL_PER; ++u) {
+    if (j0 + u < n) pk[j0 + u] = run;
+    run += l8[u];
+  }
+  if (threadIdx.x == 0) block_tot[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(PL_THREADS) plan_blocks_kernel(int64_t* __restrict__ block_tot, int64_t nb) {
+  __shared__ int64_t wsum[PL_THREADS / 32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += PL_THREADS) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t x = i < nb ? block_tot[i] : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan(x, wsum, tot);
+    if (i < nb) block_tot[i] = ex + carry;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) block_tot[nb] = carry;
+}
+
+__global__ void __launch_bounds__(PL_THREADS)
+    plan_add_kernel(int64_t* __restrict__ pk, int64_t n, const int64_t* __restrict__ block_tot, int64_t nb) {
+  const int64_t j0 = (int64_t)blockIdx.x * PL_CHUNK + (int64_t)threadIdx.x * PL_PER;
+  const int64_t add = block_tot[blockIdx.x];
+#pragma unroll
+  for (int u = 0; u < PL_PER; ++u)
+    if (j0 + u < n) pk[j0 + u] += add;
+  if (blockIdx.x == 0 && threadIdx.x == 0) pk[n] = block_tot[nb];
+}
+
+size_t packed_plan_bytes(int64_t n_cand) {
+  const int64_t nb = (n_cand + PL_CHUNK - 1) / PL_CHUNK;
+  return align_up(8 * (size_t)(n_cand + 1), 256) + align_up(8 * (size_t)n_cand, 256) +
+         align_up(4 * (size_t)n_cand, 256) + align_up(8 * (size_t)(nb + 1), 256) + 256;
+}
+
+struct TcLaunch {
+  TmapSet tm;
+  TcParams p;
+  size_t smem;
+  int grid;
+};
+
+static int prepare_tc(const cbx_batch* b, const void* d_rows, int64_t n_rows, float* scores, TcLaunch& L) {
   const int kblocks = (b->dim + 63) / 64;
   const int tile_n = kblocks <= 2 ? 128 : (kblocks <= 4 ? 64 : 32);
   const int nq = (b->max_lq + 31) / 32;
@@ -462,20 +638,23 @@ int launch_maxsim_tc(const cbx_batch* b, float* scores, cudaStream_t stream) {
   const size_t budget = 227 * 1024 - 1024 /*align slack*/ - bar_bytes - q_slot_bytes;
   int stages = (int)std::min<size_t>(TC_MAX_STAGES, budget / stage_bytes);
   if (stages < 2) return fail(CBX_EINVAL, "tcgen05 scorer: query tile too large for shared memory");
-  const size_t smem = 1024 + (size_t)q_slot_bytes + (size_t)stages * stage_bytes + bar_bytes;
-
-  CUtensorMap tmd, tmq;
-  int rc = make_tmap(&tmd, b->d_tokens, b->dtype, b->n_d_tokens, b->dim, (uint32_t)tile_n);
+  L.smem = 1024 + (size_t)q_slot_bytes + (size_t)stages * stage_bytes + bar_bytes;
+  for (int k = 0; k < 5; ++k) {
+    const int h = tile_n >> k;
+    int rc = make_tmap(&L.tm.d[k], d_rows, b->dtype, n_rows, b->dim, (uint32_t)(h >= 8 ? h : 8));
+    if (rc) return rc;
+  }
+  int rc = make_tmap(&L.tm.q, b->q_tokens, b->dtype, b->n_q_tokens, b->dim, (uint32_t)lqp);
   if (rc) return rc;
-  rc = make_tmap(&tmq, b->q_tokens, b->dtype, b->n_q_tokens, b->dim, (uint32_t)lqp);
-  if (rc) return rc;
-
-  const int nsm = sm_count();
-  TcParams p;
+  TcParams& p = L.p;
   p.q_tok_off = b->q_tok_off;
   p.d_tok_off = b->d_tok_off;
   p.q_doc_off = b->q_doc_off;
   p.scores = scores;
+  p.packed = 0;
+  p.src_row = nullptr;
+  p.doc_len = nullptr;
+  p.n_tokens_dev = nullptr;
   p.n_queries = b->n_queries;
   p.n_docs = b->n_docs;
   p.n_tokens = b->n_d_tokens;
@@ -489,12 +668,60 @@ int launch_maxsim_tc(const cbx_batch* b, float* scores, cudaStream_t stream) {
   p.clamp_negative = b->clamp_negative;
   p.q_slot_bytes = q_slot_bytes;
   p.stage_bytes = stage_bytes;
+  L.grid = (int)std::max<int64_t>(1, std::min<int64_t>(b->n_docs, sm_count()));
+  return CBX_OK;
+}
 
-  CBX_CUDA_CHECK(cudaFuncSetAttribute(maxsim_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(b->n_docs, nsm));
-  maxsim_tc_kernel<<<grid, TC_THREADS, smem, stream>>>(tmd, tmq, p);
+static int run_tc(const TcLaunch& L, cudaStream_t stream) {
+  CBX_CUDA_CHECK(cudaFuncSetAttribute(maxsim_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
+  maxsim_tc_kernel<<<L.grid, TC_THREADS, L.smem, stream>>>(L.tm, L.p);
   CBX_LAUNCH_CHECK("maxsim_tc_kernel launch");
   return CBX_OK;
+}
+
+int launch_maxsim_tc(const cbx_batch* b, float* scores, cudaStream_t stream) {
+  if (!tc_supported(b)) return fail(CBX_EINVAL, "tcgen05 scorer needs f16/bf16 tokens, Lq <= 128, dim % 8 == 0");
+  if (b->n_docs == 0 || b->n_queries == 0) return CBX_OK;
+  TcLaunch L;
+  int rc = prepare_tc(b, b->d_tokens, b->n_d_tokens, scores, L);
+  if (rc) return rc;
+  return run_tc(L, stream);
+}
+
+// Candidates of an HBM-resident corpus scored in place: b->d_tokens / n_d_tokens describe the corpus,
+// b->q_doc_off the per-query candidate ranges of cand_ids; no copy of the candidates is made.
+int launch_maxsim_tc_packed(const cbx_batch* b, const int64_t* corpus_off, int64_t n_corpus,
+                            const int64_t* cand_ids, float* scores, void* ws, size_t ws_bytes, int* status,
+                            cudaStream_t stream) {
+  if (!tc_supported(b)) return fail(CBX_EINVAL, "tcgen05 scorer needs f16/bf16 tokens, Lq <= 128, dim % 8 == 0");
+  const int64_t n = b->n_docs;
+  if (n == 0 || b->n_queries == 0) return CBX_OK;
+  if (ws_bytes < packed_plan_bytes(n)) return fail(CBX_EINVAL, "packed scorer: workspace too small");
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int64_t* pk = reinterpret_cast<int64_t*>(w);
+  w += align_up(8 * (size_t)(n + 1), 256);
+  int64_t* src = reinterpret_cast<int64_t*>(w);
+  w += align_up(8 * (size_t)n, 256);
+  int32_t* len = reinterpret_cast<int32_t*>(w);
+  w += align_up(4 * (size_t)n, 256);
+  int64_t* btot = reinterpret_cast<int64_t*>(w);
+  const int64_t nb = (n + PL_CHUNK - 1) / PL_CHUNK;
+  plan_local_kernel<<<(unsigned)nb, PL_THREADS, 0, stream>>>(corpus_off, n_corpus, cand_ids, n, pk, src, len, btot,
+                                                             status);
+  CBX_LAUNCH_CHECK("plan_local_kernel launch");
+  plan_blocks_kernel<<<1, PL_THREADS, 0, stream>>>(btot, nb);
+  CBX_LAUNCH_CHECK("plan_blocks_kernel launch");
+  plan_add_kernel<<<(unsigned)nb, PL_THREADS, 0, stream>>>(pk, n, btot, nb);
+  CBX_LAUNCH_CHECK("plan_add_kernel launch");
+  TcLaunch L;
+  int rc = prepare_tc(b, b->d_tokens, b->n_d_tokens, scores, L);
+  if (rc) return rc;
+  L.p.packed = 1;
+  L.p.d_tok_off = pk;
+  L.p.src_row = src;
+  L.p.doc_len = len;
+  L.p.n_tokens_dev = pk + n;
+  return run_tc(L, stream);
 }
 
 }  // namespace cbx

@@ -204,11 +204,37 @@ def test_resident_corpus_rerank_matches_oracle():
     co = np.concatenate([[0], np.cumsum([len(c) for c in cands])]).astype(np.int64)
     qt = torch.from_numpy(np.concatenate(queries)).pin_memory()
     k = 5
-    idx, val = corpus.rerank_topk(qt, qo, np.concatenate(cands), co, k)
     docs64 = [W.to_float64(toks[off[i]:off[i + 1]], "f16") for i in range(500)]
-    for q in range(7):
-        s, t, _ = maxsim_ref.score_query(W.to_float64(queries[q], "f16"), [docs64[c] for c in cands[q]], k)
+    for mode in ("packed", "gather"):
+        idx, val = corpus.rerank_topk(qt, qo, np.concatenate(cands), co, k, mode=mode)
+        for q in range(7):
+            s, t, _ = maxsim_ref.score_query(W.to_float64(queries[q], "f16"), [docs64[c] for c in cands[q]], k)
+            assert topk_matches(idx[q].tolist(), t, s, 1e-3), mode
+            np.testing.assert_allclose(val[q].numpy(), s[idx[q].numpy()], rtol=1e-3)
+        with pytest.raises(IndexError):
+            corpus.rerank_topk(qt, qo, np.full(int(co[-1]), 500), co, k, mode=mode)
+
+
+@pytest.mark.parametrize("dt,lq,d", [("f16", 32, 128), ("bf16", 48, 128), ("bf16", 64, 256), ("f16", 100, 96)])
+def test_packed_corpus_scores_match_oracle_on_config_shapes(dt, lq, d):
+    """Packed streaming from the corpus: per-document 8-row alignment, docs across tiles, 1-token docs."""
+    from paper_2602_02827_b200.batch import Corpus
+
+    rng = np.random.default_rng(lq + d)
+    lens = np.concatenate([[1, 7, 8, 9, 127, 128, 129, 1030, 3000], rng.integers(1, 600, size=300)])
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    toks = W._cast(W._unit(rng.standard_normal((int(off[-1]), d))), dt)
+    corpus = Corpus(toks, off, dtype=storage_dtype(dt))
+    qs = [W._cast(W._unit(rng.standard_normal((int(rng.integers(1, lq + 1)), d))), dt) for _ in range(5)]
+    cands = [rng.permutation(len(lens))[: int(rng.integers(20, 200))] for _ in range(5)]
+    from paper_2602_02827_b200.batch import to_torch_tokens
+
+    qt = torch.cat([to_torch_tokens(q, storage_dtype(dt)) for q in qs]).pin_memory()
+    qo = np.concatenate([[0], np.cumsum([q.shape[0] for q in qs])]).astype(np.int64)
+    co = np.concatenate([[0], np.cumsum([len(c) for c in cands])]).astype(np.int64)
+    idx, val = corpus.rerank_topk(qt, qo, np.concatenate(cands), co, 10)
+    docs64 = [W.to_float64(toks[off[i]:off[i + 1]], dt) for i in range(len(lens))]
+    for q in range(5):
+        s, t, _ = maxsim_ref.score_query(W.to_float64(qs[q], dt), [docs64[c] for c in cands[q]], 10)
         assert topk_matches(idx[q].tolist(), t, s, 1e-3)
-        np.testing.assert_allclose(val[q].numpy(), s[idx[q].numpy()], rtol=1e-3)
-    with pytest.raises(IndexError):
-        corpus.rerank_topk(qt, qo, np.full(int(co[-1]), 500), co, k)
+        np.testing.assert_allclose(val[q].numpy(), s[idx[q].numpy()], rtol=1e-3, atol=1e-3)
