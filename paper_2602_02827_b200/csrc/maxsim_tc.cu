@@ -35,6 +35,10 @@ constexpr int TC_EPI_WARP0 = 4;
 constexpr int TC_ACC_BUFS = 4;
 constexpr int TC_MAX_TILE_N = 128;
 constexpr int TC_MAX_STAGES = 8;
+#ifndef CBX_PACK_ALIGN
+#define CBX_PACK_ALIGN 32
+#endif
+constexpr int TC_PACK = CBX_PACK_ALIGN;  // packed-mode row granularity (power of two, >= 8)
 
 struct TcParams {
   const int64_t* q_tok_off;
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     ptx::fence_mbarrier_init();
   }
   if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tm.d[0]);
+    for (int k = 0; k < 5; ++k) ptx::prefetch_tmap(&tm.d[k]);
     ptx::prefetch_tmap(&tm.q);
   }
   if (warp == 1) ptx::tmem_alloc<TC_ACC_BUFS * TC_MAX_TILE_N>(tmem_holder);
@@ -204,15 +208,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (lane 0 issues)
-    uint32_t stage = 0, phase = 0, qphase = 0;
+  if (warp == 0 || (p.packed && (warp == 2 || warp == 3))) {
+    // ------------------------------------------------------------ TMA producers (lane 0 issues)
+    // Warp 0 loads the query and, in packed mode, shares the document tiles round-robin with warps 2
+    // and 3 (packed tiles need several small boxes each; three issuers keep the ring full).
+    const int np = p.packed ? 3 : 1;
+    const int pi = warp == 0 ? 0 : warp - 1;
+    uint32_t qphase = 0, tg = 0;
     const uint64_t pol = ptx::policy_evict_first();
     ChunkCursor cur;
     cur.init(p);
     ChunkInfo c;
     while (cur.next(p, c)) {
-      if (lane == 0) {
+      if (pi == 0 && lane == 0) {
         // one query slot: reload only after every MMA of the previous chunk retired
         ptx::mbar_wait(qempty, qphase ^ 1);
         ptx::mbar_arrive_expect_tx(qfull, (uint32_t)(p.rep * p.kblocks * p.lqp * 128));
@@ -230,17 +238,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         w_src = __ldg(p.src_row + win + lane);
         w_len = __ldg(p.doc_len + win + lane);
       }
-      for (int t = 0; t < c.ntiles; ++t) {
+      for (int t = 0; t < c.ntiles; ++t, ++tg) {
         const int64_t r0 = c.cs + (int64_t)t * p.tile_n;
         const int64_t r1 = c.ce - r0 < p.tile_n ? c.ce : r0 + p.tile_n;
-        if (lane == 0) {
+        const bool mine = (int)(tg % (uint32_t)np) == pi;
+        const uint32_t stage = tg % (uint32_t)p.stages, phase = (tg / (uint32_t)p.stages) & 1u;
+        if (lane == 0 && mine) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[stage], p.packed ? (uint32_t)((r1 - r0) * 128 * p.kblocks) : p.stage_bytes);
         }
         __syncwarp();
         uint8_t* dst = stages + (size_t)stage * p.stage_bytes;
         if (!p.packed) {
-          if (lane == 0)
+          if (lane == 0 && mine)
             for (int kb = 0; kb < p.kblocks; ++kb)
               ptx::tma_load_2d_hint(dst + kb * p.tile_n * 128, &tm.d[0], &full[stage], kb * 64, (int32_t)r0, pol);
         } else {
@@ -262,14 +272,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (pk >= r1) break;
             const int64_t src = __shfl_sync(0xffffffffu, w_src, sl);
             const int32_t len = __shfl_sync(0xffffffffu, w_len, sl);
-            const int64_t pk_next = pk + ((len + 7) & ~7);
+            const int64_t pk_next = pk + ((len + TC_PACK - 1) & ~(TC_PACK - 1));
             const int64_t ov0 = pk > r0 ? pk : r0;
             const int64_t ov1 = pk_next < r1 ? pk_next : r1;
-            if (lane == 0) {
+            if (lane == 0 && mine) {
               int64_t row = ov0, srow = src + (ov0 - pk);
               for (int k = 0; k < 5; ++k) {
                 const int h = p.tile_n >> k;
-                if (h < 8) break;
+                if (h < TC_PACK) break;
                 while (ov1 - row >= h) {
                   for (int kb = 0; kb < p.kblocks; ++kb)
                     ptx::tma_load_2d_hint(dst + kb * p.tile_n * 128 + (row - r0) * 128, &tm.d[k], &full[stage],
@@ -283,7 +293,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             ++jd;
           }
         }
-        if (++stage == (uint32_t)p.stages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -342,7 +351,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const bool lane_valid = wig * 32 + lane < c.lq;
         // window of document end offsets: ends[lane] = end of doc (win + lane); in packed mode the end
         // of the valid rows, the next document starting at the following multiple of 8
-        const int64_t align = p.packed ? 7 : 0;
+        const int64_t align = p.packed ? TC_PACK - 1 : 0;
         auto end_of = [&](int64_t d) -> int64_t {
           if (d >= c.doc1) return INT64_MAX;
           return p.packed ? __ldg(p.d_tok_off + d) + __ldg(p.doc_len + d) : __ldg(p.d_tok_off + d + 1);
@@ -570,7 +579,7 @@ __global__ void __launch_bounds__(PL_THREADS)
       }
       src_row[j] = s0;
       len[j] = (int32_t)L;
-      l8[u] = (L + 7) & ~int64_t(7);
+      l8[u] = (L + TC_PACK - 1) & ~int64_t(TC_PACK - 1);
     }
     t += l8[u];
   }
