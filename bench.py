@@ -291,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
                              "d2h_bytes_per_step": int(nq * K * 8), "ms_per_step": e_ms,
                              "api": "batch.Corpus.rerank_topk: corpus resident in HBM (fit once, untimed); per step "
                                     "H2D query tokens + candidate ids, TMA streams candidates straight from the "
-                                    "corpus (packed 8-row layout), score, Top-K, D2H Top-K; "
+                                    "corpus (32-row packed layout), score, Top-K, D2H Top-K; "
                                     "max of device-event and host wall time",
                              "topk_equals_device_path": bool(got_docs is not None and
                                                              np.array_equal(got_docs, ref_docs))}
