@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       cur.init(p);
       ChunkInfo c;
       const uint32_t q_addr = ptx::smem_u32(q_slot);
+      const uint64_t ad0 = ptx::smem_desc_sw128(q_addr);
       while (cur.next(p, c)) {
         ptx::mbar_wait(qfull, qphase);
         qphase ^= 1;
@@ -314,13 +315,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           ptx::tc_fence_after();
           const uint32_t b_addr = ptx::smem_u32(stages + (size_t)stage * p.stage_bytes);
           const uint32_t d_tmem = tmem_base + acc * TC_MAX_TILE_N;
-          for (int kb = 0; kb < p.kblocks; ++kb) {
+          // descriptors advance by (byte offset >> 4) in their 14-bit start-address field
+          const uint64_t bd0 = ptx::smem_desc_sw128(b_addr);
+          const uint32_t bstep = (uint32_t)(p.tile_n * 128) >> 4;
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4) {
-              uint64_t ad = ptx::smem_desc_sw128(q_addr + kb * 16384 + k4 * 32);
-              uint64_t bd = ptx::smem_desc_sw128(b_addr + kb * p.tile_n * 128 + k4 * 32);
-              ptx::tc_mma_f16(d_tmem, ad, bd, p.idesc, (kb | k4) != 0);
-            }
+          for (int kb = 0; kb < 8; ++kb) {
+            if (kb >= p.kblocks) break;
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4)
+              ptx::tc_mma_f16(d_tmem, ad0 + (uint64_t)(kb * 1024 + k4 * 2), bd0 + (uint64_t)(kb * bstep + k4 * 2),
+                              p.idesc, (kb | k4) != 0);
           }
           ptx::tc_commit(&empty[stage]);
           ptx::tc_commit(&tfull[acc]);
