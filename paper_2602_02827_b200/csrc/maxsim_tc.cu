@@ -208,11 +208,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  if (warp == 0 || (p.packed && (warp == 2 || warp == 3))) {
+  if (warp == 0 || (p.packed && (warp == 2 || (warp == 3 && p.stages >= 3)))) {
     // ------------------------------------------------------------ TMA producers (lane 0 issues)
     // Warp 0 loads the query and, in packed mode, shares the document tiles round-robin with warps 2
     // and 3 (packed tiles need several small boxes each; three issuers keep the ring full).
-    const int np = p.packed ? 3 : 1;
+    // a producer may only run one ring lap ahead of the slowest one: np <= stages keeps every
+    // empty-barrier parity wait unambiguous
+    const int np = p.packed ? (p.stages < 3 ? p.stages : 3) : 1;
     const int pi = warp == 0 ? 0 : warp - 1;
     uint32_t qphase = 0, tg = 0;
     const uint64_t pol = ptx::policy_evict_first();
@@ -640,7 +642,7 @@ struct TcLaunch {
 
 static int prepare_tc(const cbx_batch* b, const void* d_rows, int64_t n_rows, float* scores, TcLaunch& L) {
   const int kblocks = (b->dim + 63) / 64;
-  const int tile_n = kblocks <= 2 ? 128 : (kblocks <= 4 ? 64 : 32);
+  const int tile_n = kblocks <= 4 ? 128 : 32;  // d <= 256: N=128 MMAs; d=512: 32 rows (smem)
   const int nq = (b->max_lq + 31) / 32;
   const int rep = nq == 3 ? 1 : 4 / nq;
   const int lqp = nq * 32;
