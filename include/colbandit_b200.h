@@ -159,6 +159,28 @@ CBX_API int cbx_corpus_rerank_topk(const cbx_batch* b, const int64_t* corpus_off
                                    float* topk_val, int* status, void* workspace, size_t ws_bytes,
                                    void* stream);
 
+/* ---------------------------------------------------------------- Stage 1 */
+/* Stage-1 candidate scan, replaces colbandit/pipeline.py:105-158
+ * (generate_candidates): for every query-token row r of b->q_tokens (rows of
+ * all queries, in order; n_q_tokens rows) and the corpus b->d_tokens
+ * (n_d_tokens rows; offsets / q_doc_off are not used), the k_prime corpus
+ * tokens of highest float64 similarity (floored at 0 if clamp_negative),
+ * ranked by (-similarity, corpus token index) like np.lexsort (pipeline.py:137):
+ * nb_tok[r * k_prime + j] = corpus token index, nb_val[...] = similarity.
+ * path CBX_PATH_TC (f16/bf16, dim <= 256, k_prime <= 64, >= 8192 corpus
+ * tokens) scans once with tcgen05 and refines in float64; it needs
+ * corpus_norm_max (cbx_token_norm_max) and, after the stream completes,
+ * status[0] != 0 means "re-run with CBX_PATH_SIMT" (list overflow or zero
+ * ties under clamping). CBX_PATH_SIMT is float64 on the CUDA cores (any
+ * dtype). 1 <= k_prime <= min(8192, n_d_tokens); n_q_tokens <= 65535. */
+CBX_API size_t cbx_stage1_workspace_bytes(const cbx_batch* b, int k_prime, int path);
+CBX_API int cbx_stage1_topk(const cbx_batch* b, int k_prime, int path, float corpus_norm_max,
+                            int64_t* nb_tok, double* nb_val, int* status, void* workspace,
+                            size_t ws_bytes, void* stream);
+/* *out = max over rows of the L2 norm of a token matrix (rounded up to float). */
+CBX_API int cbx_token_norm_max(const void* tokens, int64_t n_tokens, int dim, int dtype, float* out,
+                               void* stream);
+
 /* ---------------------------------------------------------------- P2 */
 /* numpy PCG64 bit-generator state (np.random.default_rng(seed)
  * .bit_generator.state): 128-bit state and increment plus the buffered

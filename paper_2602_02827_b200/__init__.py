@@ -5,6 +5,8 @@ Public surface mirrors the reference package's hot-path entry points:
 * ``Similarity``, ``QueryTokens``, ``DocTokens``, ``MaxSimOracle`` (oracle.py)
 * ``BanditConfig``, ``RunResult``, ``run`` (bandit.py); ``full_rerank`` (baselines.py)
 * ``RadiusConfig``, ``CellBounds`` (bounds.py)
+* ``generate_candidates``, ``derive_bounds``, ``CandidateSet``, ... (pipeline.py: Stage 1 on the device)
+* ``ColBanditReranker``, ``RerankOutcome`` (reranker.py: the estimator facade)
 
 plus batched device entry points (``TokenBatch``, ``rerank_topk``,
 ``maxsim_scores``, ``run_batch``). All arithmetic runs in libcbx.so
@@ -18,3 +20,6 @@ from .baselines import full_rerank  # noqa: F401
 from .batch import TokenBatch, exact_cells, maxsim_scores, rerank_topk, topk  # noqa: F401
 from .bounds import CellBounds, RadiusConfig, fp_correction  # noqa: F401
 from .oracle import DocTokens, MaxSimOracle, QueryTokens, Similarity  # noqa: F401
+from .pipeline import (CandidateSet, TokenNeighbor, TokenNeighborList, derive_bounds,  # noqa: F401
+                       generate_candidates, load_candidates, save_candidates)
+from .reranker import ColBanditReranker, RerankOutcome  # noqa: F401

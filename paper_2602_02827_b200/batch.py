@@ -85,6 +85,7 @@ class TokenBatch:
         b = cls(q_tokens, q_tok_off, d_tokens, d_tok_off, q_doc_off, bool(clamp_negative),
                 int(lq.max()) if len(lq) else 0, int(ndocs.max()) if len(ndocs) else 0,
                 int(qtoks.max()) if len(qtoks) else 0)
+        b.host_offsets = (qo, do, qd)
         b._validate()
         return b
 
@@ -319,7 +320,82 @@ class Corpus:
         self.lengths = np.diff(off)
         self.offsets = torch.from_numpy(off).cuda()
         self.clamp_negative = bool(clamp_negative)
+        self.doc_ids = None
         self._ws = {}
+        self._norm_max = None
+
+    @classmethod
+    def from_docs(cls, docs, clamp_negative: bool = False) -> "Corpus":
+        """Upload a list of DocTokens (or token matrices) once; mixed dtypes widen to the widest one."""
+        import torch
+
+        from .oracle import DocTokens
+
+        stores = [d._store if isinstance(d, DocTokens) else to_torch_tokens(d) for d in docs]
+        if not stores:
+            raise ValueError("corpus must contain at least one document")
+        dts = {t.dtype for t in stores}
+        if len(dts) > 1:
+            order = [torch.float16, torch.bfloat16, torch.float32, torch.float64]
+            wide = max(dts, key=order.index)
+            if dts == {torch.float16, torch.bfloat16}:
+                wide = torch.float32
+            stores = [t.to(wide) for t in stores]
+        off = np.zeros(len(stores) + 1, np.int64)
+        np.cumsum([t.shape[0] for t in stores], out=off[1:])
+        c = cls(torch.cat([t.cpu() for t in stores]).contiguous(), off, clamp_negative=clamp_negative)
+        c.doc_ids = [d.doc_id if isinstance(d, DocTokens) else f"doc{i:04d}" for i, d in enumerate(docs)]
+        return c
+
+    @property
+    def n_tokens(self) -> int:
+        return int(self.tokens.shape[0])
+
+    def widened(self, dtype) -> "Corpus":
+        """A cached copy of this corpus in a wider dtype (for queries the storage dtype cannot hold exactly)."""
+        key = ("wide", dtype)
+        c = self._ws.get(key)
+        if c is None:
+            c = Corpus(self.tokens.to(dtype), self.offsets_host, clamp_negative=self.clamp_negative)
+            c.doc_ids = self.doc_ids
+            self._ws[key] = c
+        return c
+
+    def norm_max(self) -> float:
+        """Largest token L2 norm (device reduction, computed once; bounds the tcgen05 Stage-1 error)."""
+        if self._norm_max is None:
+            import torch
+
+            out = torch.zeros(1, dtype=torch.float32, device=self.tokens.device)
+            lib = _lib.load()
+            _lib.check(lib.cbx_token_norm_max(self.tokens.data_ptr(), self.n_tokens, self.dim,
+                                              dtype_code(self.tokens.dtype), out.data_ptr(),
+                                              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                       "token_norm_max")
+            self._norm_max = float(out.item())
+        return self._norm_max
+
+    def gather(self, cand_ids):
+        """Pack corpus documents ``cand_ids`` (int64, host) into contiguous device rows + CSR offsets."""
+        import torch
+
+        lib = _lib.load()
+        cid = np.ascontiguousarray(np.asarray(cand_ids, dtype=np.int64))
+        if len(cid) and (cid.min() < 0 or cid.max() >= self.n_docs):
+            raise IndexError(f"candidate id out of range [0, {self.n_docs})")
+        total = int(self.lengths[cid].sum()) if len(cid) else 0
+        rows = torch.empty((max(total, 1), self.dim), dtype=self.tokens.dtype, device=self.tokens.device)[:total]
+        doff = torch.zeros(len(cid) + 1, dtype=torch.int64, device=self.tokens.device)
+        status = torch.zeros(1, dtype=torch.int32, device=self.tokens.device)
+        dcid = torch.from_numpy(cid).to(self.tokens.device)
+        _lib.check(lib.cbx_gather_candidates(self.tokens.data_ptr(), self.offsets.data_ptr(), self.n_docs, self.dim,
+                                             dtype_code(self.tokens.dtype), dcid.data_ptr(), len(cid),
+                                             rows.data_ptr(), total, doff.data_ptr(), status.data_ptr(),
+                                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "gather")
+        host_off = np.zeros(len(cid) + 1, np.int64)
+        if len(cid):
+            np.cumsum(self.lengths[cid], out=host_off[1:])
+        return rows, doff, host_off
 
     @property
     def n_docs(self) -> int:

@@ -73,22 +73,23 @@ __global__ void __launch_bounds__(GA_SCAN_THREADS)
   }
 }
 
-// one warp per candidate: copy its token rows (16-byte vectors, coalesced)
+// one warp per candidate: copy its token rows (16-byte vectors when rows allow, else 2-byte words; coalesced)
+template <typename V>
 __global__ void __launch_bounds__(GA_COPY_THREADS)
-    gather_copy_kernel(const uint4* __restrict__ corpus, const int64_t* __restrict__ corpus_off,
+    gather_copy_kernel(const V* __restrict__ corpus, const int64_t* __restrict__ corpus_off,
                        const int64_t* __restrict__ cand, int64_t n_cand, const int64_t* __restrict__ out_off,
-                       uint4* __restrict__ out, int64_t row_vecs, int64_t n_corpus) {
+                       V* __restrict__ out, int64_t row_vecs, int64_t n_corpus) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (GA_COPY_THREADS / 32);
   for (int64_t j = (int64_t)blockIdx.x * (GA_COPY_THREADS / 32) + (threadIdx.x >> 5); j < n_cand; j += warps) {
     const int64_t id = cand[j];
     if (id < 0 || id >= n_corpus) continue;
-    const uint4* src = corpus + corpus_off[id] * row_vecs;
-    uint4* dst = out + out_off[j] * row_vecs;
+    const V* src = corpus + corpus_off[id] * row_vecs;
+    V* dst = out + out_off[j] * row_vecs;
     const int64_t n = (out_off[j + 1] - out_off[j]) * row_vecs;
     int64_t v = lane;
     for (; v + 96 < n; v += 128) {
-      const uint4 a = __ldg(src + v), b = __ldg(src + v + 32), c = __ldg(src + v + 64), d = __ldg(src + v + 96);
+      const V a = __ldg(src + v), b = __ldg(src + v + 32), c = __ldg(src + v + 64), d = __ldg(src + v + 96);
       dst[v] = a;
       dst[v + 32] = b;
       dst[v + 64] = c;
@@ -110,21 +111,24 @@ int cbx_gather_candidates(const void* corpus_tokens, const int64_t* corpus_doc_o
   if (n_cand <= 0) return CBX_OK;
   const size_t es = dtype_size(dtype);
   if (!es) return fail(CBX_EINVAL, "gather: unknown dtype");
-  if ((dim * es) % 16) return fail(CBX_EINVAL, "gather: token rows must be a multiple of 16 bytes");
   if (!corpus_tokens || !corpus_doc_off || !cand_ids || !out_tokens || !out_doc_off || !status)
     return fail(CBX_EINVAL, "gather: NULL buffer");
-  if ((reinterpret_cast<uintptr_t>(corpus_tokens) | reinterpret_cast<uintptr_t>(out_tokens)) & 15)
-    return fail(CBX_EINVAL, "gather: token buffers must be 16-byte aligned");
   (void)out_capacity;  // the caller sized out_tokens from host-side candidate lengths
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   gather_scan_kernel<<<1, GA_SCAN_THREADS, 0, st>>>(corpus_doc_off, n_corpus_docs, cand_ids, n_cand, out_doc_off,
                                                       status);
   CBX_LAUNCH_CHECK("gather_scan_kernel launch");
-  const int64_t row_vecs = (int64_t)dim * es / 16;
   const int grid = (int)std::min<int64_t>((n_cand + 7) / 8, (int64_t)sm_count() * 16);
-  gather_copy_kernel<<<grid, GA_COPY_THREADS, 0, st>>>(static_cast<const uint4*>(corpus_tokens), corpus_doc_off,
-                                                       cand_ids, n_cand, out_doc_off,
-                                                       static_cast<uint4*>(out_tokens), row_vecs, n_corpus_docs);
+  const bool vec16 = ((dim * es) % 16 == 0) &&
+                     !((reinterpret_cast<uintptr_t>(corpus_tokens) | reinterpret_cast<uintptr_t>(out_tokens)) & 15);
+  if (vec16)
+    gather_copy_kernel<uint4><<<grid, GA_COPY_THREADS, 0, st>>>(
+        static_cast<const uint4*>(corpus_tokens), corpus_doc_off, cand_ids, n_cand, out_doc_off,
+        static_cast<uint4*>(out_tokens), (int64_t)dim * es / 16, n_corpus_docs);
+  else
+    gather_copy_kernel<uint16_t><<<grid, GA_COPY_THREADS, 0, st>>>(
+        static_cast<const uint16_t*>(corpus_tokens), corpus_doc_off, cand_ids, n_cand, out_doc_off,
+        static_cast<uint16_t*>(out_tokens), (int64_t)dim * es / 2, n_corpus_docs);
   CBX_LAUNCH_CHECK("gather_copy_kernel launch");
   return CBX_OK;
 }

@@ -512,7 +512,7 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-static int make_tmap(CUtensorMap* m, const void* base, int dtype, int64_t rows, int32_t dim, uint32_t box_rows) {
+int make_tmap(CUtensorMap* m, const void* base, int dtype, int64_t rows, int32_t dim, uint32_t box_rows) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return fail(CBX_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)dim, (cuuint64_t)(rows > 0 ? rows : 1)};

@@ -1,0 +1,713 @@
+// Stage-1 candidate scan — replaces colbandit/pipeline.py:105-158 (generate_candidates).
+//
+// For every query-token row r and the whole corpus (T token rows), the k'
+// corpus tokens of highest similarity, ranked by (-similarity, global token
+// index) exactly like np.lexsort((arange(T), -scores[:, t]))[:k'] on the
+// reference's float64 scores (pipeline.py:137), similarity floored at 0 under
+// clamp_negative (oracle.py:65-66). Two device paths, identical results:
+//
+// * SIMT (any dtype): the corpus is cut into chunks; a CUDA-core kernel writes
+//   float64 similarities of a chunk (same fma order as the exact cell kernel,
+//   so a neighbour's value equals the cell the oracle later reveals), the
+//   segmented bitonic Top-K keeps k' per row and chunk, a last Top-K merges
+//   the chunk winners (chunk order = token order, so ties stay lowest-index).
+//
+// * TC (fp16/bf16, large corpora): one persistent TMA + tcgen05 scan streams
+//   the corpus once per 128 query rows (query rows = the MMA's M, 128 corpus
+//   tokens = N, fp32 accumulators in TMEM). The epilogue keeps, per row, a
+//   running k'-th best value theta (sorted top-k' in shared memory) and
+//   appends every token with fp32 value >= theta - 2*eps_r to a per-(item,
+//   row) list; eps_r = dim * 2^-19 * |q_r| * max_j |e_j| bounds the fp32
+//   accumulation error (products of 16-bit inputs are exact). A refine kernel
+//   per row takes T_f = the k'-th best fp32 value over all items, recomputes
+//   every listed token with fp32 >= T_f - 2*eps_r in float64 and sorts them by
+//   (-value, index). Every true Top-k' token has fp32 >= T_f - 2*eps_r, so the
+//   result is exact. Overflowing a list, or a k'-th value of exactly 0 under
+//   clamping (zero ties resolved by corpus order), sets status: the caller
+//   re-runs the SIMT path.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace cbx {
+
+int make_tmap(CUtensorMap* m, const void* base, int dtype, int64_t rows, int32_t dim, uint32_t box_rows);
+size_t topk_workspace_bytes(int64_t n_queries, int64_t max_q_docs, int K);
+int launch_topk_f64(const double* s, const int64_t* off, int64_t nq, int64_t mx, int K, int32_t* ti, double* tv,
+                    void* ws, size_t wb, cudaStream_t st);
+
+template <typename T>
+using S1Store = typename std::conditional<std::is_same<T, double>::value, double, float>::type;
+
+// ============================================================ SIMT path
+constexpr int SX_ROWS = 64, SX_TOKS = 64, SX_THREADS = 256;
+
+// sims[r * C + j] = <e_{c0+j}, q_r> (float64, clamped), -inf for j >= cn (chunk padding)
+template <typename T>
+__global__ void __launch_bounds__(SX_THREADS)
+    stage1_sims_kernel(const T* __restrict__ q, int64_t R, const T* __restrict__ d, int64_t c0, int64_t cn,
+                       int64_t C, int dim, int clamp, double* __restrict__ sims) {
+  using S = S1Store<T>;
+  extern __shared__ __align__(16) uint8_t sx_smem[];
+  const int dp = dim + 1;
+  S* qs = reinterpret_cast<S*>(sx_smem);
+  S* ts = qs + SX_ROWS * dp;
+  const int64_t r0 = (int64_t)blockIdx.y * SX_ROWS, j0 = (int64_t)blockIdx.x * SX_TOKS;
+  for (int i = threadIdx.x; i < SX_ROWS * dim; i += SX_THREADS) {
+    const int r = i / dim, k = i - r * dim;
+    qs[r * dp + k] = r0 + r < R ? (S)Elem<T>::to_d(q[(r0 + r) * dim + k]) : (S)0;
+    ts[r * dp + k] = j0 + r < cn ? (S)Elem<T>::to_d(d[(c0 + j0 + r) * dim + k]) : (S)0;
+  }
+  __syncthreads();
+  const int j = threadIdx.x & (SX_TOKS - 1), rg = threadIdx.x / SX_TOKS;  // rows rg + 4 i
+  double acc[SX_ROWS / 4];
+#pragma unroll
+  for (int i = 0; i < SX_ROWS / 4; ++i) acc[i] = 0.0;
+  for (int k = 0; k < dim; ++k) {
+    const double e = (double)ts[j * dp + k];
+#pragma unroll
+    for (int i = 0; i < SX_ROWS / 4; ++i) acc[i] = fma(e, (double)qs[(rg + 4 * i) * dp + k], acc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < SX_ROWS / 4; ++i) {
+    const int64_t r = r0 + rg + 4 * i;
+    if (r >= R) break;
+    double v = acc[i];
+    if (clamp) v = v > 0.0 ? v : 0.0;
+    sims[r * C + j0 + j] = j0 + j < cn ? v : -INFINITY;
+  }
+}
+
+__global__ void stage1_offsets_kernel(int64_t* off, int64_t n, int64_t stride) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+    off[i] = i * stride;
+}
+
+// chunk winners -> candidate list [r][chunk * kp + i] (value, global token index)
+__global__ void stage1_scatter_kernel(const int32_t* __restrict__ idx, const double* __restrict__ val, int64_t R,
+                                      int kp, int64_t chunk, int64_t nch, int64_t c0, double* __restrict__ cv,
+                                      int64_t* __restrict__ ct) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R * kp; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / kp, s = i - r * kp;
+    cv[r * nch * kp + chunk * kp + s] = val[i];
+    ct[r * nch * kp + chunk * kp + s] = c0 + idx[i];
+  }
+}
+
+__global__ void stage1_final_kernel(const int32_t* __restrict__ pos, const double* __restrict__ val,
+                                    const int64_t* __restrict__ ct, int64_t R, int kp, int64_t width,
+                                    int64_t* __restrict__ nb_tok, double* __restrict__ nb_val) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R * kp; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / kp;
+    nb_tok[i] = ct[r * width + pos[i]];
+    nb_val[i] = val[i];
+  }
+}
+
+struct SxPlan {
+  int64_t C, nch;
+  size_t o_sims, o_off1, o_off2, o_idx, o_val, o_cv, o_ct, o_pos, o_fval, o_tk, total;
+};
+
+static SxPlan plan_simt(int64_t R, int64_t T, int kp) {
+  SxPlan p;
+  int64_t C = std::max<int64_t>(4096, ((int64_t)1 << 25) / std::max<int64_t>(R, 1));
+  C = std::max<int64_t>(C, 2 * (int64_t)kp);
+  C = std::min<int64_t>(C, (T + SX_TOKS - 1) / SX_TOKS * SX_TOKS);
+  C = std::max<int64_t>(C, (int64_t)kp);
+  C = (C + SX_TOKS - 1) / SX_TOKS * SX_TOKS;
+  p.C = C;
+  p.nch = (T + C - 1) / C;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += align_up(bytes, 256);
+    return at;
+  };
+  p.o_sims = take(8 * (size_t)R * C);
+  p.o_off1 = take(8 * (size_t)(R + 1));
+  p.o_off2 = take(8 * (size_t)(R + 1));
+  p.o_idx = take(4 * (size_t)R * kp);
+  p.o_val = take(8 * (size_t)R * kp);
+  p.o_cv = take(8 * (size_t)R * p.nch * kp);
+  p.o_ct = take(8 * (size_t)R * p.nch * kp);
+  p.o_pos = take(4 * (size_t)R * kp);
+  p.o_fval = take(8 * (size_t)R * kp);
+  p.o_tk = take(std::max(topk_workspace_bytes(R, C, kp), topk_workspace_bytes(R, p.nch * kp, kp)));
+  p.total = o;
+  return p;
+}
+
+template <typename T>
+static int run_simt(const cbx_batch* b, int kp, int64_t* nb_tok, double* nb_val, uint8_t* ws, cudaStream_t st) {
+  using S = S1Store<T>;
+  const int64_t R = b->n_q_tokens, Tn = b->n_d_tokens;
+  SxPlan p = plan_simt(R, Tn, kp);
+  double* sims = reinterpret_cast<double*>(ws + p.o_sims);
+  int64_t* off1 = reinterpret_cast<int64_t*>(ws + p.o_off1);
+  int64_t* off2 = reinterpret_cast<int64_t*>(ws + p.o_off2);
+  int32_t* idx = reinterpret_cast<int32_t*>(ws + p.o_idx);
+  double* val = reinterpret_cast<double*>(ws + p.o_val);
+  double* cv = reinterpret_cast<double*>(ws + p.o_cv);
+  int64_t* ct = reinterpret_cast<int64_t*>(ws + p.o_ct);
+  int32_t* pos = reinterpret_cast<int32_t*>(ws + p.o_pos);
+  double* fval = reinterpret_cast<double*>(ws + p.o_fval);
+  void* tk = ws + p.o_tk;
+  const size_t tk_bytes = p.total - p.o_tk;
+  const size_t smem = 2 * sizeof(S) * SX_ROWS * (b->dim + 1);
+  if (smem > 227 * 1024) return fail(CBX_EINVAL, "stage-1 SIMT scan: embedding dim too large");
+  CBX_CUDA_CHECK(cudaFuncSetAttribute(stage1_sims_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  stage1_offsets_kernel<<<64, 256, 0, st>>>(off1, R, p.C);
+  stage1_offsets_kernel<<<64, 256, 0, st>>>(off2, R, p.nch * kp);
+  CBX_LAUNCH_CHECK("stage1_offsets_kernel launch");
+  const int sgrid = (int)std::min<int64_t>((R * kp + 255) / 256, 4096);
+  for (int64_t c = 0; c < p.nch; ++c) {
+    const int64_t c0 = c * p.C, cn = std::min<int64_t>(p.C, Tn - c0);
+    dim3 grid((unsigned)(p.C / SX_TOKS), (unsigned)((R + SX_ROWS - 1) / SX_ROWS));
+    stage1_sims_kernel<T><<<grid, SX_THREADS, smem, st>>>(static_cast<const T*>(b->q_tokens), R,
+                                                           static_cast<const T*>(b->d_tokens), c0, cn, p.C, b->dim,
+                                                           b->clamp_negative, sims);
+    CBX_LAUNCH_CHECK("stage1_sims_kernel launch");
+    if (p.nch == 1) {  // one chunk: its winners are the answer (chunk positions == token indices)
+      int rc = launch_topk_f64(sims, off1, R, p.C, kp, idx, val, tk, tk_bytes, st);
+      if (rc) return rc;
+      stage1_scatter_kernel<<<sgrid, 256, 0, st>>>(idx, val, R, kp, 0, 1, 0, nb_val, nb_tok);
+      CBX_LAUNCH_CHECK("stage1_scatter_kernel launch");
+      return CBX_OK;
+    }
+    int rc = launch_topk_f64(sims, off1, R, p.C, kp, idx, val, tk, tk_bytes, st);
+    if (rc) return rc;
+    stage1_scatter_kernel<<<sgrid, 256, 0, st>>>(idx, val, R, kp, c, p.nch, c0, cv, ct);
+    CBX_LAUNCH_CHECK("stage1_scatter_kernel launch");
+  }
+  int rc = launch_topk_f64(cv, off2, R, p.nch * kp, kp, pos, fval, tk, tk_bytes, st);
+  if (rc) return rc;
+  stage1_final_kernel<<<sgrid, 256, 0, st>>>(pos, fval, ct, R, kp, p.nch * kp, nb_tok, nb_val);
+  CBX_LAUNCH_CHECK("stage1_final_kernel launch");
+  return CBX_OK;
+}
+
+// ============================================================ TC path
+constexpr int S1_THREADS = 256;
+constexpr int S1_EPI_WARP0 = 4;
+constexpr int S1_ACC = 4;
+constexpr int S1_TILE = 128;
+constexpr int S1_MAX_STAGES = 6;
+constexpr int S1_MAX_KP = 64;
+constexpr int S1_FCAP = 2048;  // refined candidates per row
+constexpr int S1_MIN_TOKENS = 8192;
+
+struct S1Params {
+  int64_t R, T;
+  int32_t RB, P, NT, kp, cap, kblocks, stages;  // cap: list entries per (item, row)
+  int32_t tile_n;                               // corpus tokens per MMA tile (N): 128, or 64 for d > 128 when needed
+  uint32_t idesc, q_slot_bytes, stage_bytes;
+  const float* eps;
+  int32_t* cnt;   // [items][128]
+  uint2* ent;     // [items][128][cap]: (fp32 bits, token)
+  float* topv;    // [items][128][kp] descending, -inf padded
+  int* status;
+};
+
+__global__ void stage1_eps_kernel(const void* q, int dtype, int64_t R, int dim, float norm_max, float* eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= R) return;
+  double s = 0.0;
+  for (int k = lane; k < dim; k += 32) {
+    double x = dtype == CBX_BF16 ? (double)__bfloat162float(static_cast<const __nv_bfloat16*>(q)[r * dim + k])
+                                 : (double)__half2float(static_cast<const __half*>(q)[r * dim + k]);
+    s += x * x;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) eps[r] = (float)((double)dim * 0x1p-19 * sqrt(s) * (double)norm_max * 1.0001 + 1e-30);
+}
+
+__device__ __forceinline__ float s1_max32(const float (&v)[32], int n) {
+  float m = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j < n) m = fmaxf(m, v[j]);
+  return m;
+}
+
+__global__ void __launch_bounds__(S1_THREADS, 1)
+    stage1_scan_kernel(const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_q,
+                       S1Params p) {
+  extern __shared__ __align__(1024) uint8_t s1_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s1_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* q_slot = smem;
+  uint8_t* stages = smem + p.q_slot_bytes;
+  float* tops = reinterpret_cast<float*>(stages + (size_t)p.stages * p.stage_bytes);  // [kp][128]
+  float* scratch = tops + (size_t)p.kp * 128;                                          // [32][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + 32 * 128);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S1_MAX_STAGES;
+  uint64_t* qfull = bars + 2 * S1_MAX_STAGES;
+  uint64_t* qempty = qfull + 1;
+  uint64_t* tfull = qempty + 1;
+  uint64_t* tempty = tfull + S1_ACC;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + S1_ACC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int items = p.RB * p.P;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(qfull, 1);
+    ptx::mbar_init(qempty, 1);
+    for (int s = 0; s < S1_ACC; ++s) {
+      ptx::mbar_init(&tfull[s], 1);
+      ptx::mbar_init(&tempty[s], 4);
+    }
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tm_d);
+    ptx::prefetch_tmap(&tm_q);
+  }
+  if (warp == 1) ptx::tmem_alloc<S1_ACC * S1_TILE>(tmem_holder);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_first();
+      uint32_t tg = 0, qphase = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int rb = item / p.P, pp = item - rb * p.P;
+        const int t0 = (int)((int64_t)p.NT * pp / p.P), t1 = (int)((int64_t)p.NT * (pp + 1) / p.P);
+        ptx::mbar_wait(qempty, qphase ^ 1);
+        qphase ^= 1;
+        ptx::mbar_arrive_expect_tx(qfull, (uint32_t)(p.kblocks * 16384));
+        for (int kb = 0; kb < p.kblocks; ++kb) ptx::tma_load_2d(q_slot + kb * 16384, &tm_q, qfull, kb * 64, rb * 128);
+        for (int t = t0; t < t1; ++t, ++tg) {
+          const uint32_t stage = tg % (uint32_t)p.stages, ph = (tg / (uint32_t)p.stages) & 1u;
+          ptx::mbar_wait(&empty[stage], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], p.stage_bytes);
+          uint8_t* dst = stages + (size_t)stage * p.stage_bytes;
+          for (int kb = 0; kb < p.kblocks; ++kb)
+            ptx::tma_load_2d_hint(dst + kb * p.tile_n * 128, &tm_d, &full[stage], kb * 64, t * p.tile_n, pol);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t tg = 0, qphase = 0, stage = 0, phase = 0;
+      const uint64_t ad0 = ptx::smem_desc_sw128(ptx::smem_u32(q_slot));
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int rb = item / p.P, pp = item - rb * p.P;
+        const int t0 = (int)((int64_t)p.NT * pp / p.P), t1 = (int)((int64_t)p.NT * (pp + 1) / p.P);
+        ptx::mbar_wait(qfull, qphase);
+        qphase ^= 1;
+        ptx::tc_fence_after();
+        for (int t = t0; t < t1; ++t, ++tg) {
+          const uint32_t acc = tg & (S1_ACC - 1);
+          ptx::mbar_wait(&tempty[acc], ((tg >> 2) & 1) ^ 1);
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint64_t bd0 = ptx::smem_desc_sw128(ptx::smem_u32(stages + (size_t)stage * p.stage_bytes));
+          const uint32_t d_tmem = tmem_base + acc * S1_TILE;
+          const uint32_t bstep = (uint32_t)(p.tile_n * 128) >> 4;
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb) {
+            if (kb >= p.kblocks) break;
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4)
+              ptx::tc_mma_f16(d_tmem, ad0 + (uint64_t)(kb * 1024 + k4 * 2), bd0 + (uint64_t)(kb * bstep + k4 * 2),
+                              p.idesc, (kb | k4) != 0);
+          }
+          ptx::tc_commit(&empty[stage]);
+          ptx::tc_commit(&tfull[acc]);
+          if (++stage == (uint32_t)p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::tc_commit(qempty);
+      }
+    }
+  } else if (warp >= S1_EPI_WARP0) {
+    const int quad = warp - S1_EPI_WARP0;
+    const int rl = quad * 32 + lane;  // row within the 128-row block == TMEM lane
+    const uint32_t tmem_lane = (uint32_t)(quad * 32) << 16;
+    uint32_t tg = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      const int rb = item / p.P, pp = item - rb * p.P;
+      const int t0 = (int)((int64_t)p.NT * pp / p.P), t1 = (int)((int64_t)p.NT * (pp + 1) / p.P);
+      const int64_t r = (int64_t)rb * 128 + rl;
+      const bool valid = r < p.R;
+      const float eps2 = valid ? 2.0f * __ldg(p.eps + r) : 0.0f;
+      float theta = -INFINITY, thr = -INFINITY;
+      int ntop = 0, cnt = 0;
+      bool ovf = false;
+      uint2* mylist = p.ent + ((size_t)item * 128 + rl) * p.cap;
+      for (int t = t0; t < t1; ++t, ++tg) {
+        const uint32_t acc = tg & (S1_ACC - 1);
+        ptx::mbar_wait(&tfull[acc], (tg >> 2) & 1);
+        ptx::tc_fence_after();
+        float v[4][32];
+        const uint32_t taddr = tmem_base + tmem_lane + acc * S1_TILE;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (b * 32 < p.tile_n) ptx::tmem_ld_32x32b_x32(taddr + b * 32, v[b]);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        const int64_t tb = (int64_t)t * p.tile_n;
+        const int ncols = p.T - tb < p.tile_n ? (int)(p.T - tb) : p.tile_n;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int nb = ncols - b * 32;
+          if (nb <= 0) break;
+          const float m = nb >= 32 ? s1_max32(v[b], 32) : s1_max32(v[b], nb);
+          if (!(valid && m >= thr)) continue;
+          // rare: spill this lane's 32 values and walk them (keeps the insertion code out of the unrolled body)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) scratch[j * 128 + rl] = v[b][j];
+          const int jn = nb < 32 ? nb : 32;
+          for (int j = 0; j < jn; ++j) {
+            const float x = scratch[j * 128 + rl];
+            if (!(x >= thr)) continue;
+            if (cnt < p.cap) mylist[cnt++] = make_uint2(__float_as_uint(x), (uint32_t)(tb + b * 32 + j));
+            else ovf = true;
+            if (ntop < p.kp || x > theta) {
+              int s = ntop < p.kp ? ntop : p.kp - 1;
+              while (s > 0 && tops[(s - 1) * 128 + rl] < x) {
+                tops[s * 128 + rl] = tops[(s - 1) * 128 + rl];
+                --s;
+              }
+              tops[s * 128 + rl] = x;
+              if (ntop < p.kp) ++ntop;
+              if (ntop == p.kp) {
+                theta = tops[(p.kp - 1) * 128 + rl];
+                thr = theta - eps2;
+              }
+            }
+          }
+        }
+      }
+      if (valid) {
+        p.cnt[(size_t)item * 128 + rl] = cnt;
+        float* tv = p.topv + ((size_t)item * 128 + rl) * p.kp;
+        for (int s = 0; s < p.kp; ++s) tv[s] = s < ntop ? tops[s * 128 + rl] : -INFINITY;
+        if (ovf) atomicOr(p.status, 1);
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<S1_ACC * S1_TILE>(tmem_base);
+  }
+}
+
+constexpr int S1R_THREADS = 512;
+
+template <typename T>
+__global__ void __launch_bounds__(S1R_THREADS)
+    stage1_refine_kernel(const T* __restrict__ q, const T* __restrict__ d, S1Params p, int dim, int clamp,
+                         int64_t* __restrict__ nb_tok, double* __restrict__ nb_val) {
+  extern __shared__ __align__(16) uint8_t rf_smem[];
+  __shared__ int n_f;
+  __shared__ int ovf;
+  const int64_t r = blockIdx.x;
+  const int rb = (int)(r / 128), rl = (int)(r % 128);
+  const int n = p.P * p.kp;
+  int S = 32;
+  while (S < n) S <<= 1;
+  float* sv = reinterpret_cast<float*>(rf_smem);                  // [S] (<= 16384)
+  uint64_t* fkey = reinterpret_cast<uint64_t*>(rf_smem);          // reused after the threshold: [S1_FCAP]
+  uint32_t* ftok = reinterpret_cast<uint32_t*>(fkey + S1_FCAP);   // [S1_FCAP]
+  float* qs = reinterpret_cast<float*>(ftok + S1_FCAP);           // [dim]
+  if (threadIdx.x == 0) {
+    n_f = 0;
+    ovf = 0;
+  }
+  for (int i = threadIdx.x; i < S; i += S1R_THREADS) {
+    float x = -INFINITY;
+    if (i < n) {
+      const int it = rb * p.P + i / p.kp;
+      x = p.topv[((size_t)it * 128 + rl) * p.kp + i % p.kp];
+    }
+    sv[i] = x;
+  }
+  __syncthreads();
+  for (int k = 2; k <= S; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < S; i += S1R_THREADS) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const float a = sv[i], b2 = sv[ixj];
+          const bool desc = (i & k) == 0;
+          if (desc ? a < b2 : a > b2) {
+            sv[i] = b2;
+            sv[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  const float thr = sv[p.kp - 1] - 2.0f * p.eps[r];
+  __syncthreads();  // sv is overwritten below
+  for (int pp = 0; pp < p.P; ++pp) {
+    const size_t it = (size_t)rb * p.P + pp;
+    const int c = p.cnt[it * 128 + rl];
+    const uint2* lst = p.ent + (it * 128 + rl) * p.cap;
+    for (int e = threadIdx.x; e < c; e += S1R_THREADS) {
+      const uint2 u = lst[e];
+      if (__uint_as_float(u.x) >= thr) {
+        const int s = atomicAdd(&n_f, 1);
+        if (s < S1_FCAP) ftok[s] = u.y;
+        else ovf = 1;
+      }
+    }
+  }
+  for (int k = threadIdx.x; k < dim; k += S1R_THREADS) qs[k] = Elem<T>::to_f(q[r * dim + k]);
+  __syncthreads();
+  const int nf = n_f < S1_FCAP ? n_f : S1_FCAP;
+  int SF = 32;
+  while (SF < nf) SF <<= 1;
+  for (int i = threadIdx.x; i < SF; i += S1R_THREADS) {
+    if (i < nf) {
+      const T* e = d + (size_t)ftok[i] * dim;
+      double acc = 0.0;
+      for (int k = 0; k < dim; ++k) acc = fma(Elem<T>::to_d(__ldg(e + k)), (double)qs[k], acc);
+      if (clamp) acc = acc > 0.0 ? acc : 0.0;
+      fkey[i] = desc_key_f64(acc);
+    } else {
+      fkey[i] = ~0ull;
+      ftok[i] = 0xFFFFFFFFu;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= SF; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < SF; i += S1R_THREADS) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t a = fkey[i], b2 = fkey[ixj];
+          const uint32_t ia = ftok[i], ib = ftok[ixj];
+          const bool a_gt = a > b2 || (a == b2 && ia > ib);
+          if (((i & k) == 0) == a_gt) {
+            fkey[i] = b2;
+            fkey[ixj] = a;
+            ftok[i] = ib;
+            ftok[ixj] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < p.kp; i += S1R_THREADS) {
+    const uint64_t u = ~fkey[i];
+    const uint64_t bits = (u & 0x8000000000000000ull) ? (u & 0x7FFFFFFFFFFFFFFFull) : ~u;
+    const double v = __longlong_as_double((long long)bits);
+    nb_tok[r * p.kp + i] = ftok[i];
+    nb_val[r * p.kp + i] = v;
+    if (i == p.kp - 1 && clamp && v == 0.0) atomicOr(p.status, 2);  // zero ties: corpus order decides
+  }
+  if (threadIdx.x == 0 && (ovf || nf < p.kp)) atomicOr(p.status, 1);
+}
+
+struct TcPlan {
+  int RB, P, NT, kblocks, stages, items, cap, tile_n;
+  size_t smem, o_eps, o_cnt, o_ent, o_topv, total;
+};
+
+static bool tc_eligible(const cbx_batch* b, int kp) {
+  return (b->dtype == CBX_F16 || b->dtype == CBX_BF16) && b->dim % 8 == 0 && b->dim <= 256 && kp <= S1_MAX_KP &&
+         b->n_d_tokens >= S1_MIN_TOKENS && b->n_d_tokens < (int64_t(1) << 31) && b->n_q_tokens < (int64_t(1) << 24);
+}
+
+static int plan_tc(const cbx_batch* b, int kp, TcPlan& t) {
+  const int64_t R = b->n_q_tokens, Tn = b->n_d_tokens;
+  t.RB = (int)((R + 127) / 128);
+  t.kblocks = (b->dim + 63) / 64;
+  const size_t qb = (size_t)t.kblocks * 16384;
+  const size_t fixed = 1024 + qb + 4 * (size_t)kp * 128 + 4 * 32 * 128 + 8 * 32;
+  const size_t budget = 227 * 1024 - fixed;
+  t.tile_n = budget / ((size_t)t.kblocks * 16384) >= 3 ? 128 : 64;  // keep >= 3 stages in flight
+  const size_t sb = (size_t)t.kblocks * t.tile_n * 128;
+  t.stages = (int)std::min<size_t>(S1_MAX_STAGES, budget / sb);
+  if (t.stages < 2) return fail(CBX_EINVAL, "stage-1 scan: tile does not fit shared memory");
+  t.NT = (int)((Tn + t.tile_n - 1) / t.tile_n);
+  const int G = sm_count();
+  t.P = t.RB >= G ? 1 : std::min(t.NT, (G + t.RB - 1) / t.RB);
+  t.items = t.RB * t.P;
+  t.smem = fixed + (size_t)t.stages * sb;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += align_up(bytes, 256);
+    return at;
+  };
+  t.o_eps = take(4 * (size_t)R);
+  t.o_cnt = take(4 * (size_t)t.items * 128);
+  // expected appends per list ~ kp * (1 + ln(tokens per item / kp)); overflow falls back to SIMT
+  t.cap = std::min(1024, std::max(256, 12 * kp));
+  t.o_ent = take(8 * (size_t)t.items * 128 * t.cap);
+  t.o_topv = take(4 * (size_t)t.items * 128 * kp);
+  t.total = o;
+  return CBX_OK;
+}
+
+template <typename T>
+static int run_tc(const cbx_batch* b, int kp, float norm_max, int64_t* nb_tok, double* nb_val, int* status,
+                  uint8_t* ws, cudaStream_t st) {
+  TcPlan t;
+  int rc = plan_tc(b, kp, t);
+  if (rc) return rc;
+  S1Params p;
+  p.R = b->n_q_tokens;
+  p.T = b->n_d_tokens;
+  p.RB = t.RB;
+  p.P = t.P;
+  p.NT = t.NT;
+  p.kp = kp;
+  p.cap = t.cap;
+  p.kblocks = t.kblocks;
+  p.stages = t.stages;
+  p.tile_n = t.tile_n;
+  p.idesc = ptx::idesc_f16(b->dtype == CBX_BF16, 128, (uint32_t)t.tile_n);
+  p.q_slot_bytes = (uint32_t)(t.kblocks * 16384);
+  p.stage_bytes = (uint32_t)(t.kblocks * t.tile_n * 128);
+  p.eps = reinterpret_cast<float*>(ws + t.o_eps);
+  p.cnt = reinterpret_cast<int32_t*>(ws + t.o_cnt);
+  p.ent = reinterpret_cast<uint2*>(ws + t.o_ent);
+  p.topv = reinterpret_cast<float*>(ws + t.o_topv);
+  p.status = status;
+  CUtensorMap tm_d, tm_q;
+  rc = make_tmap(&tm_d, b->d_tokens, b->dtype, b->n_d_tokens, b->dim, (uint32_t)t.tile_n);
+  if (rc) return rc;
+  rc = make_tmap(&tm_q, b->q_tokens, b->dtype, b->n_q_tokens, b->dim, 128);
+  if (rc) return rc;
+  stage1_eps_kernel<<<(unsigned)((p.R + 7) / 8), 256, 0, st>>>(b->q_tokens, b->dtype, p.R, b->dim, norm_max,
+                                                               const_cast<float*>(p.eps));
+  CBX_LAUNCH_CHECK("stage1_eps_kernel launch");
+  CBX_CUDA_CHECK(cudaFuncSetAttribute(stage1_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
+  const int grid = std::min(t.items, sm_count());
+  stage1_scan_kernel<<<grid, S1_THREADS, t.smem, st>>>(tm_d, tm_q, p);
+  CBX_LAUNCH_CHECK("stage1_scan_kernel launch");
+  int S = 32;
+  while (S < t.P * kp) S <<= 1;
+  const size_t rsmem = std::max<size_t>(4 * (size_t)S, 12 * (size_t)S1_FCAP + 4 * (size_t)b->dim);
+  CBX_CUDA_CHECK(cudaFuncSetAttribute(stage1_refine_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
+  stage1_refine_kernel<T><<<(unsigned)p.R, S1R_THREADS, rsmem, st>>>(
+      static_cast<const T*>(b->q_tokens), static_cast<const T*>(b->d_tokens), p, b->dim, b->clamp_negative, nb_tok,
+      nb_val);
+  CBX_LAUNCH_CHECK("stage1_refine_kernel launch");
+  return CBX_OK;
+}
+
+// ============================================================ corpus norm
+template <typename T>
+__global__ void token_norm_max_kernel(const T* __restrict__ x, int64_t n, int dim, unsigned int* out_bits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  float best = 0.0f;
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5); r < n; r += warps) {
+    double s = 0.0;
+    for (int k = lane; k < dim; k += 32) {
+      const double v = Elem<T>::to_d(x[r * dim + k]);
+      s += v * v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    best = fmaxf(best, __double2float_ru(sqrt(s)));
+  }
+  if (lane == 0) atomicMax(out_bits, __float_as_uint(best));  // non-negative floats order like their bits
+}
+
+static int resolve_path(const cbx_batch* b, int kp, int path) {
+  if (path == CBX_PATH_AUTO) return tc_eligible(b, kp) ? CBX_PATH_TC : CBX_PATH_SIMT;
+  return path;
+}
+
+static int check_stage1(const cbx_batch* b, int kp) {
+  if (!b) return fail(CBX_EINVAL, "batch descriptor is NULL");
+  if (kp < 1) return fail(CBX_EINVAL, "k_prime must be at least 1, got " + std::to_string(kp));
+  if (b->n_q_tokens < 1 || b->n_d_tokens < 1) return fail(CBX_EINVAL, "stage-1 scan needs query rows and corpus tokens");
+  if (kp > b->n_d_tokens) return fail(CBX_EINVAL, "k_prime exceeds the corpus token count");
+  if (kp > 8192) return fail(CBX_EINVAL, "k_prime > 8192 is not supported");
+  if (b->n_q_tokens > 65535) return fail(CBX_EINVAL, "stage-1 scan: at most 65535 query rows per call");
+  if (b->dim <= 0 || dtype_size(b->dtype) == 0) return fail(CBX_EINVAL, "bad dim / dtype");
+  if (!b->q_tokens || !b->d_tokens) return fail(CBX_EINVAL, "token buffers are NULL");
+  return CBX_OK;
+}
+
+}  // namespace cbx
+
+using namespace cbx;
+
+extern "C" {
+
+size_t cbx_stage1_workspace_bytes(const cbx_batch* b, int k_prime, int path) {
+  if (check_stage1(b, k_prime)) return 0;
+  path = resolve_path(b, k_prime, path);
+  if (path == CBX_PATH_TC) {
+    TcPlan t;
+    if (plan_tc(b, k_prime, t)) return 0;
+    return t.total;
+  }
+  return plan_simt(b->n_q_tokens, b->n_d_tokens, k_prime).total;
+}
+
+int cbx_stage1_topk(const cbx_batch* b, int k_prime, int path, float corpus_norm_max, int64_t* nb_tok,
+                    double* nb_val, int* status, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_stage1(b, k_prime);
+  if (rc) return rc;
+  if (!nb_tok || !nb_val || !status) return fail(CBX_EINVAL, "stage-1 output buffers are NULL");
+  path = resolve_path(b, k_prime, path);
+  if (path != CBX_PATH_TC && path != CBX_PATH_SIMT) return fail(CBX_EINVAL, "unknown stage-1 path");
+  if (path == CBX_PATH_TC && !tc_eligible(b, k_prime))
+    return fail(CBX_EINVAL, "stage-1 tcgen05 path needs f16/bf16, dim % 8 == 0, dim <= 256, k_prime <= 64 and a "
+                            "corpus of at least 8192 tokens");
+  if (path == CBX_PATH_TC && !(corpus_norm_max > 0.0f && corpus_norm_max < INFINITY))
+    return fail(CBX_EINVAL, "stage-1 tcgen05 path needs the corpus max token norm (cbx_token_norm_max)");
+  if (ws_bytes < cbx_stage1_workspace_bytes(b, k_prime, path)) return fail(CBX_EINVAL, "stage-1 workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  CBX_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(int), st));
+  if (path == CBX_PATH_TC) {
+    if (b->dtype == CBX_F16) return run_tc<__half>(b, k_prime, corpus_norm_max, nb_tok, nb_val, status, w, st);
+    return run_tc<__nv_bfloat16>(b, k_prime, corpus_norm_max, nb_tok, nb_val, status, w, st);
+  }
+  switch (b->dtype) {
+    case CBX_F32: return run_simt<float>(b, k_prime, nb_tok, nb_val, w, st);
+    case CBX_F64: return run_simt<double>(b, k_prime, nb_tok, nb_val, w, st);
+    case CBX_F16: return run_simt<__half>(b, k_prime, nb_tok, nb_val, w, st);
+    case CBX_BF16: return run_simt<__nv_bfloat16>(b, k_prime, nb_tok, nb_val, w, st);
+  }
+  return fail(CBX_EINVAL, "unknown dtype");
+}
+
+int cbx_token_norm_max(const void* tokens, int64_t n_tokens, int dim, int dtype, float* out, void* stream) {
+  if (!tokens || !out || n_tokens < 1 || dim < 1) return fail(CBX_EINVAL, "token_norm_max: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CBX_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(float), st));
+  unsigned int* bits = reinterpret_cast<unsigned int*>(out);
+  const int grid = (int)std::min<int64_t>((n_tokens + 7) / 8, (int64_t)sm_count() * 8);
+  switch (dtype) {
+    case CBX_F32: token_norm_max_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(tokens), n_tokens, dim, bits); break;
+    case CBX_F64: token_norm_max_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(tokens), n_tokens, dim, bits); break;
+    case CBX_F16: token_norm_max_kernel<__half><<<grid, 256, 0, st>>>(static_cast<const __half*>(tokens), n_tokens, dim, bits); break;
+    case CBX_BF16:
+      token_norm_max_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(tokens), n_tokens, dim, bits);
+      break;
+    default: return fail(CBX_EINVAL, "unknown dtype");
+  }
+  CBX_LAUNCH_CHECK("token_norm_max_kernel launch");
+  return CBX_OK;
+}
+
+}  // extern "C"
