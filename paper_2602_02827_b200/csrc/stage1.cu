@@ -18,7 +18,10 @@
 //   running k'-th best value theta (sorted top-k' in shared memory) and
 //   appends every token with fp32 value >= theta - 2*eps_r to a per-(item,
 //   row) list; eps_r = dim * 2^-19 * |q_r| * max_j |e_j| bounds the fp32
-//   accumulation error (products of 16-bit inputs are exact). A refine kernel
+//   accumulation error (products of 16-bit inputs are exact). theta starts
+//   from a pre-pass over every stride-th tile (the k'-th best of a corpus
+//   sample is a lower bound on the global k'-th value), so the main scan
+//   appends and inserts almost only true contenders. A refine kernel
 //   per row takes T_f = the k'-th best fp32 value over all items, recomputes
 //   every listed token with fp32 >= T_f - 2*eps_r in float64 and sorts them by
 //   (-value, index). Every true Top-k' token has fp32 >= T_f - 2*eps_r, so the
@@ -201,9 +204,13 @@ constexpr int S1_MIN_TOKENS = 8192;
 struct S1Params {
   int64_t R, T;
   int32_t RB, P, NT, kp, cap, kblocks, stages;  // cap: list entries per (item, row)
+  int32_t sample;   // 1: threshold pre-pass over every stride-th tile (tops only, no lists)
+  int32_t stride;   // tile stride of the visited sequence
+  int32_t NS;       // tiles in the visited sequence
   int32_t tile_n;                               // corpus tokens per MMA tile (N): 128, or 64 for d > 128 when needed
   uint32_t idesc, q_slot_bytes, stage_bytes;
   const float* eps;
+  unsigned int* gthr;  // [R] order-preserving keys of the best published k'-th value per row
   int32_t* cnt;   // [items][128]
   uint2* ent;     // [items][128][cap]: (fp32 bits, token)
   float* topv;    // [items][128][kp] descending, -inf padded
@@ -225,12 +232,30 @@ __global__ void stage1_eps_kernel(const void* q, int dtype, int64_t R, int dim, 
   if (lane == 0) eps[r] = (float)((double)dim * 0x1p-19 * sqrt(s) * (double)norm_max * 1.0001 + 1e-30);
 }
 
-__device__ __forceinline__ float s1_max32(const float (&v)[32], int n) {
-  float m = -INFINITY;
+// order-preserving float <-> uint keys (atomicMax on floats of any sign)
+__device__ __forceinline__ unsigned int ord_key(float x) {
+  const unsigned int u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord_val(unsigned int k) {
+  if (k == 0u) return -INFINITY;  // nothing published yet
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+__device__ __forceinline__ float s1_fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// max of 32 register values as a 3-input tree (depth 4)
+__device__ __forceinline__ float s1_tree_max32(const float (&v)[32]) {
+  float a[11];
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (j < n) m = fmaxf(m, v[j]);
-  return m;
+  for (int i = 0; i < 10; ++i) a[i] = s1_fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+  a[10] = fmaxf(v[30], v[31]);
+  const float b0 = s1_fmax3(a[0], a[1], a[2]), b1 = s1_fmax3(a[3], a[4], a[5]), b2 = s1_fmax3(a[6], a[7], a[8]);
+  return s1_fmax3(s1_fmax3(b0, b1, b2), a[9], a[10]);
 }
 
 __global__ void __launch_bounds__(S1_THREADS, 1)
@@ -282,7 +307,7 @@ __global__ void __launch_bounds__(S1_THREADS, 1)
       uint32_t tg = 0, qphase = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const int rb = item / p.P, pp = item - rb * p.P;
-        const int t0 = (int)((int64_t)p.NT * pp / p.P), t1 = (int)((int64_t)p.NT * (pp + 1) / p.P);
+        const int t0 = (int)((int64_t)p.NS * pp / p.P), t1 = (int)((int64_t)p.NS * (pp + 1) / p.P);
         ptx::mbar_wait(qempty, qphase ^ 1);
         qphase ^= 1;
         ptx::mbar_arrive_expect_tx(qfull, (uint32_t)(p.kblocks * 16384));
@@ -293,7 +318,8 @@ __global__ void __launch_bounds__(S1_THREADS, 1)
           ptx::mbar_arrive_expect_tx(&full[stage], p.stage_bytes);
           uint8_t* dst = stages + (size_t)stage * p.stage_bytes;
           for (int kb = 0; kb < p.kblocks; ++kb)
-            ptx::tma_load_2d_hint(dst + kb * p.tile_n * 128, &tm_d, &full[stage], kb * 64, t * p.tile_n, pol);
+            ptx::tma_load_2d_hint(dst + kb * p.tile_n * 128, &tm_d, &full[stage], kb * 64, t * p.stride * p.tile_n,
+                                  pol);
         }
       }
     }
@@ -303,7 +329,7 @@ __global__ void __launch_bounds__(S1_THREADS, 1)
       const uint64_t ad0 = ptx::smem_desc_sw128(ptx::smem_u32(q_slot));
       for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const int rb = item / p.P, pp = item - rb * p.P;
-        const int t0 = (int)((int64_t)p.NT * pp / p.P), t1 = (int)((int64_t)p.NT * (pp + 1) / p.P);
+        const int t0 = (int)((int64_t)p.NS * pp / p.P), t1 = (int)((int64_t)p.NS * (pp + 1) / p.P);
         ptx::mbar_wait(qfull, qphase);
         qphase ^= 1;
         ptx::tc_fence_after();
@@ -340,11 +366,16 @@ __global__ void __launch_bounds__(S1_THREADS, 1)
     uint32_t tg = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       const int rb = item / p.P, pp = item - rb * p.P;
-      const int t0 = (int)((int64_t)p.NT * pp / p.P), t1 = (int)((int64_t)p.NT * (pp + 1) / p.P);
+      const int t0 = (int)((int64_t)p.NS * pp / p.P), t1 = (int)((int64_t)p.NS * (pp + 1) / p.P);
       const int64_t r = (int64_t)rb * 128 + rl;
       const bool valid = r < p.R;
       const float eps2 = valid ? 2.0f * __ldg(p.eps + r) : 0.0f;
-      float theta = -INFINITY, thr = -INFINITY;
+      const bool any_valid = (int64_t)rb * 128 + quad * 32 < p.R;  // warp-uniform: this quadrant holds rows
+      // theta: k'-th best fp32 value of this item's row so far (sorted tops); gtheta: the pre-pass's k'-th
+      // best over a strided sample of the corpus. Both are <= the global k'-th fp32 value, so
+      // thr = max(theta, gtheta) - 2 eps never drops a token the refine needs.
+      const float gtheta = (!p.sample && valid) ? ord_val(__ldg(p.gthr + r)) : -INFINITY;
+      float theta = -INFINITY, thr = gtheta - eps2;
       int ntop = 0, cnt = 0;
       bool ovf = false;
       uint2* mylist = p.ent + ((size_t)item * 128 + rl) * p.cap;
@@ -354,48 +385,66 @@ __global__ void __launch_bounds__(S1_THREADS, 1)
         ptx::tc_fence_after();
         float v[4][32];
         const uint32_t taddr = tmem_base + tmem_lane + acc * S1_TILE;
+        if (any_valid) {
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if (b * 32 < p.tile_n) ptx::tmem_ld_32x32b_x32(taddr + b * 32, v[b]);
-        ptx::tmem_ld_wait();
+          for (int b = 0; b < 4; ++b)
+            if (b * 32 < p.tile_n) ptx::tmem_ld_32x32b_x32(taddr + b * 32, v[b]);
+          ptx::tmem_ld_wait();
+        }
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-        const int64_t tb = (int64_t)t * p.tile_n;
+        if (!any_valid) continue;
+        const int64_t tb = (int64_t)t * p.stride * p.tile_n;
         const int ncols = p.T - tb < p.tile_n ? (int)(p.T - tb) : p.tile_n;
+        if (ncols < p.tile_n) {  // the corpus's last tile: padding columns never qualify
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int nb = ncols - b * 32;
-          if (nb <= 0) break;
-          const float m = nb >= 32 ? s1_max32(v[b], 32) : s1_max32(v[b], nb);
-          if (!(valid && m >= thr)) continue;
-          // rare: spill this lane's 32 values and walk them (keeps the insertion code out of the unrolled body)
+          for (int b = 0; b < 4; ++b)
 #pragma unroll
-          for (int j = 0; j < 32; ++j) scratch[j * 128 + rl] = v[b][j];
-          const int jn = nb < 32 ? nb : 32;
-          for (int j = 0; j < jn; ++j) {
-            const float x = scratch[j * 128 + rl];
-            if (!(x >= thr)) continue;
-            if (cnt < p.cap) mylist[cnt++] = make_uint2(__float_as_uint(x), (uint32_t)(tb + b * 32 + j));
-            else ovf = true;
-            if (ntop < p.kp || x > theta) {
-              int s = ntop < p.kp ? ntop : p.kp - 1;
-              while (s > 0 && tops[(s - 1) * 128 + rl] < x) {
-                tops[s * 128 + rl] = tops[(s - 1) * 128 + rl];
-                --s;
+            for (int j = 0; j < 32; ++j)
+              if (b * 32 + j >= ncols) v[b][j] = -INFINITY;
+        }
+        float m = fmaxf(s1_tree_max32(v[0]), s1_tree_max32(v[1]));
+        if (p.tile_n == 128) m = fmaxf(m, fmaxf(s1_tree_max32(v[2]), s1_tree_max32(v[3])));
+        if (valid && m >= thr) {
+          // rare: visit only the qualifying columns of each block
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            if (b * 32 >= ncols) break;
+            uint32_t mask = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) mask |= (b * 32 + j < ncols && v[b][j] >= thr) ? (1u << j) : 0u;
+            if (!mask) continue;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) scratch[j * 128 + rl] = v[b][j];
+            while (mask) {
+              const int j = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const float x = scratch[j * 128 + rl];
+              if (!(x >= thr)) continue;  // thr rose since the mask was built
+              if (!p.sample) {
+                if (cnt < p.cap) mylist[cnt++] = make_uint2(__float_as_uint(x), (uint32_t)(tb + b * 32 + j));
+                else ovf = true;
               }
-              tops[s * 128 + rl] = x;
-              if (ntop < p.kp) ++ntop;
-              if (ntop == p.kp) {
-                theta = tops[(p.kp - 1) * 128 + rl];
-                thr = theta - eps2;
+              if (ntop < p.kp || x > theta) {
+                int s = ntop < p.kp ? ntop : p.kp - 1;
+                while (s > 0 && tops[(s - 1) * 128 + rl] < x) {
+                  tops[s * 128 + rl] = tops[(s - 1) * 128 + rl];
+                  --s;
+                }
+                tops[s * 128 + rl] = x;
+                if (ntop < p.kp) ++ntop;
+                if (ntop == p.kp) {
+                  theta = tops[(p.kp - 1) * 128 + rl];
+                  thr = fmaxf(theta, gtheta) - eps2;
+                }
               }
             }
           }
         }
       }
       if (valid) {
-        p.cnt[(size_t)item * 128 + rl] = cnt;
+        if (!p.sample) p.cnt[(size_t)item * 128 + rl] = cnt;
         float* tv = p.topv + ((size_t)item * 128 + rl) * p.kp;
         for (int s = 0; s < p.kp; ++s) tv[s] = s < ntop ? tops[s * 128 + rl] : -INFINITY;
         if (ovf) atomicOr(p.status, 1);
@@ -412,6 +461,48 @@ __global__ void __launch_bounds__(S1_THREADS, 1)
 }
 
 constexpr int S1R_THREADS = 512;
+
+// descending bitonic sort of S (power of two) floats in shared memory by the whole CTA
+__device__ __forceinline__ void block_sort_desc(float* sv, int S) {
+  for (int k = 2; k <= S; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < S; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const float a = sv[i], b2 = sv[ixj];
+          if (((i & k) == 0) ? a < b2 : a > b2) {
+            sv[i] = b2;
+            sv[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// gthr[r] = key of the k'-th best fp32 value the threshold pre-pass saw for row r (distinct sample tokens,
+// so a lower bound on the global k'-th value); 0 if the sample held fewer than k' tokens
+__global__ void __launch_bounds__(S1R_THREADS) stage1_seed_kernel(S1Params p) {
+  extern __shared__ __align__(16) uint8_t sd_smem[];
+  float* sv = reinterpret_cast<float*>(sd_smem);
+  const int64_t r = blockIdx.x;
+  const int rb = (int)(r / 128), rl = (int)(r % 128);
+  const int n = p.P * p.kp;
+  int S = 32;
+  while (S < n) S <<= 1;
+  for (int i = threadIdx.x; i < S; i += S1R_THREADS) {
+    float x = -INFINITY;
+    if (i < n) x = p.topv[(((size_t)rb * p.P + i / p.kp) * 128 + rl) * p.kp + i % p.kp];
+    sv[i] = x;
+  }
+  __syncthreads();
+  block_sort_desc(sv, S);
+  if (threadIdx.x == 0) {
+    const float x = sv[p.kp - 1];
+    p.gthr[r] = x > -INFINITY ? ord_key(x) : 0u;
+  }
+}
+
 
 template <typename T>
 __global__ void __launch_bounds__(S1R_THREADS)
@@ -442,21 +533,7 @@ __global__ void __launch_bounds__(S1R_THREADS)
     sv[i] = x;
   }
   __syncthreads();
-  for (int k = 2; k <= S; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < S; i += S1R_THREADS) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const float a = sv[i], b2 = sv[ixj];
-          const bool desc = (i & k) == 0;
-          if (desc ? a < b2 : a > b2) {
-            sv[i] = b2;
-            sv[ixj] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
+  block_sort_desc(sv, S);
   const float thr = sv[p.kp - 1] - 2.0f * p.eps[r];
   __syncthreads();  // sv is overwritten below
   for (int pp = 0; pp < p.P; ++pp) {
@@ -521,7 +598,7 @@ __global__ void __launch_bounds__(S1R_THREADS)
 
 struct TcPlan {
   int RB, P, NT, kblocks, stages, items, cap, tile_n;
-  size_t smem, o_eps, o_cnt, o_ent, o_topv, total;
+  size_t smem, o_eps, o_gthr, o_cnt, o_ent, o_topv, total;
 };
 
 static bool tc_eligible(const cbx_batch* b, int kp) {
@@ -552,6 +629,7 @@ static int plan_tc(const cbx_batch* b, int kp, TcPlan& t) {
     return at;
   };
   t.o_eps = take(4 * (size_t)R);
+  t.o_gthr = take(4 * (size_t)R);
   t.o_cnt = take(4 * (size_t)t.items * 128);
   // expected appends per list ~ kp * (1 + ln(tokens per item / kp)); overflow falls back to SIMT
   t.cap = std::min(1024, std::max(256, 12 * kp));
@@ -582,6 +660,7 @@ static int run_tc(const cbx_batch* b, int kp, float norm_max, int64_t* nb_tok, d
   p.q_slot_bytes = (uint32_t)(t.kblocks * 16384);
   p.stage_bytes = (uint32_t)(t.kblocks * t.tile_n * 128);
   p.eps = reinterpret_cast<float*>(ws + t.o_eps);
+  p.gthr = reinterpret_cast<unsigned int*>(ws + t.o_gthr);
   p.cnt = reinterpret_cast<int32_t*>(ws + t.o_cnt);
   p.ent = reinterpret_cast<uint2*>(ws + t.o_ent);
   p.topv = reinterpret_cast<float*>(ws + t.o_topv);
@@ -595,8 +674,30 @@ static int run_tc(const cbx_batch* b, int kp, float norm_max, int64_t* nb_tok, d
                                                                const_cast<float*>(p.eps));
   CBX_LAUNCH_CHECK("stage1_eps_kernel launch");
   CBX_CUDA_CHECK(cudaFuncSetAttribute(stage1_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
-  const int grid = std::min(t.items, sm_count());
-  stage1_scan_kernel<<<grid, S1_THREADS, t.smem, st>>>(tm_d, tm_q, p);
+  const int G = sm_count();
+  // threshold pre-pass over every stride-th tile (~16 tiles per CTA): seeds each row's filter with the
+  // k'-th best of a corpus sample, so the main scan appends / inserts almost only true contenders
+  const int stride = t.NT / (G * 16);
+  if (stride >= 2) {
+    S1Params ps = p;
+    ps.sample = 1;
+    ps.stride = stride;
+    ps.NS = (t.NT + stride - 1) / stride;
+    ps.P = t.RB >= G ? 1 : std::min(ps.NS, (G + t.RB - 1) / t.RB);
+    stage1_scan_kernel<<<std::min(t.RB * ps.P, G), S1_THREADS, t.smem, st>>>(tm_d, tm_q, ps);
+    CBX_LAUNCH_CHECK("stage1_scan_kernel (pre-pass) launch");
+    int S = 32;
+    while (S < ps.P * kp) S <<= 1;
+    CBX_CUDA_CHECK(cudaFuncSetAttribute(stage1_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * S));
+    stage1_seed_kernel<<<(unsigned)p.R, S1R_THREADS, 4 * S, st>>>(ps);
+    CBX_LAUNCH_CHECK("stage1_seed_kernel launch");
+  } else {
+    CBX_CUDA_CHECK(cudaMemsetAsync(p.gthr, 0, 4 * (size_t)p.R, st));  // key 0: no seed
+  }
+  p.sample = 0;
+  p.stride = 1;
+  p.NS = t.NT;
+  stage1_scan_kernel<<<std::min(t.items, G), S1_THREADS, t.smem, st>>>(tm_d, tm_q, p);
   CBX_LAUNCH_CHECK("stage1_scan_kernel launch");
   int S = 32;
   while (S < t.P * kp) S <<= 1;

@@ -88,6 +88,8 @@ def test_generate_candidates_matches_reference_golden(path):
     ("f16", 256, 40_000, 64, 64, False, 0.0),
     ("bf16", 64, 30_000, 128, 1, True, 0.2),
     ("f16", 96, 20_000, 7, 33, False, 0.3),       # dim not a multiple of 64, heavy duplication
+    ("bf16", 64, 700_000, 40, 10, True, 0.01),    # large enough for the threshold pre-pass
+    ("f16", 128, 900_000, 200, 5, False, 0.0),    # pre-pass with two row blocks
 ])
 def test_tc_scan_equals_simt_scan(dt, d, n_tok, rows, kp, clamp, dup):
     from paper_2602_02827_b200.batch import Corpus
