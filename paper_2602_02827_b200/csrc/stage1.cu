@@ -204,7 +204,7 @@ constexpr int S1_MIN_TOKENS = 8192;
 struct S1Params {
   int64_t R, T;
   int32_t RB, P, NT, kp, cap, kblocks, stages;  // cap: list entries per (item, row)
-  int32_t sample;   // 1: threshold pre-pass over every stride-th tile (tops only, no lists)
+  int32_t sample;   // 1: threshold pre-pass over every stride-th tile (tile maxima only)
   int32_t stride;   // tile stride of the visited sequence
   int32_t NS;       // tiles in the visited sequence
   int32_t tile_n;                               // corpus tokens per MMA tile (N): 128, or 64 for d > 128 when needed
@@ -214,6 +214,7 @@ struct S1Params {
   int32_t* cnt;   // [items][128]
   uint2* ent;     // [items][128][cap]: (fp32 bits, token)
   float* topv;    // [items][128][kp] descending, -inf padded
+  float* tmax;    // pre-pass: [NS][R] tile maxima
   int* status;
 };
 
@@ -406,6 +407,10 @@ __global__ void __launch_bounds__(S1_THREADS, 1)
         }
         float m = fmaxf(s1_tree_max32(v[0]), s1_tree_max32(v[1]));
         if (p.tile_n == 128) m = fmaxf(m, fmaxf(s1_tree_max32(v[2]), s1_tree_max32(v[3])));
+        if (p.sample) {  // pre-pass: tile maxima only (distinct tokens of disjoint tiles)
+          if (valid) p.tmax[(size_t)t * p.R + r] = m;
+          continue;
+        }
         if (valid && m >= thr) {
           // rare: visit only the qualifying columns of each block
 #pragma unroll
@@ -422,10 +427,8 @@ __global__ void __launch_bounds__(S1_THREADS, 1)
               mask &= mask - 1;
               const float x = scratch[j * 128 + rl];
               if (!(x >= thr)) continue;  // thr rose since the mask was built
-              if (!p.sample) {
-                if (cnt < p.cap) mylist[cnt++] = make_uint2(__float_as_uint(x), (uint32_t)(tb + b * 32 + j));
-                else ovf = true;
-              }
+              if (cnt < p.cap) mylist[cnt++] = make_uint2(__float_as_uint(x), (uint32_t)(tb + b * 32 + j));
+              else ovf = true;
               if (ntop < p.kp || x > theta) {
                 int s = ntop < p.kp ? ntop : p.kp - 1;
                 while (s > 0 && tops[(s - 1) * 128 + rl] < x) {
@@ -443,8 +446,8 @@ __global__ void __launch_bounds__(S1_THREADS, 1)
           }
         }
       }
-      if (valid) {
-        if (!p.sample) p.cnt[(size_t)item * 128 + rl] = cnt;
+      if (valid && !p.sample) {
+        p.cnt[(size_t)item * 128 + rl] = cnt;
         float* tv = p.topv + ((size_t)item * 128 + rl) * p.kp;
         for (int s = 0; s < p.kp; ++s) tv[s] = s < ntop ? tops[s * 128 + rl] : -INFINITY;
         if (ovf) atomicOr(p.status, 1);
@@ -462,47 +465,67 @@ __global__ void __launch_bounds__(S1_THREADS, 1)
 
 constexpr int S1R_THREADS = 512;
 
-// descending bitonic sort of S (power of two) floats in shared memory by the whole CTA
-__device__ __forceinline__ void block_sort_desc(float* sv, int S) {
-  for (int k = 2; k <= S; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < S; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const float a = sv[i], b2 = sv[ixj];
-          if (((i & k) == 0) ? a < b2 : a > b2) {
-            sv[i] = b2;
-            sv[ixj] = a;
-          }
-        }
-      }
-      __syncthreads();
+// k-th largest (1-based) of n floats in shared memory: MSB-first radix select on order-preserving keys,
+// 8 bits per pass (4 passes, 256-bin shared histogram). Every thread of the CTA returns the value.
+__device__ float block_kth_largest(const float* sv, int n, int k, unsigned int* hist, unsigned int* bc) {
+  unsigned int prefix = 0u, mask = 0u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned int key = ord_key(sv[i]);
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
     }
+    __syncthreads();
+    if (warp == 0) {
+      // lane l owns bins [8l, 8l + 8); suffix sums from the top bin down
+      unsigned int c[8], tot = 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[lane * 8 + j];
+        tot += c[j];
+      }
+      unsigned int incl = tot;  // inclusive suffix sum over lanes >= this one
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int y = __shfl_down_sync(0xffffffffu, incl, o);
+        if (lane + o < 32) incl += y;
+      }
+      const unsigned int above = incl - tot;  // count in bins owned by higher lanes
+      const unsigned int kk = (unsigned int)k;
+      if (above < kk && kk <= above + tot) {  // the k-th largest falls in this lane's bins
+        unsigned int acc = above;
+        int d = 7;
+        for (; d > 0; --d) {
+          if (acc + c[d] >= kk) break;
+          acc += c[d];
+        }
+        bc[0] = (unsigned int)(lane * 8 + d);
+        bc[1] = kk - acc;
+      }
+    }
+    __syncthreads();
+    prefix |= bc[0] << shift;
+    mask |= 255u << shift;
+    k = (int)bc[1];
+    __syncthreads();
+  }
+  return ord_val(prefix);
 }
 
-// gthr[r] = key of the k'-th best fp32 value the threshold pre-pass saw for row r (distinct sample tokens,
-// so a lower bound on the global k'-th value); 0 if the sample held fewer than k' tokens
+// gthr[r] = key of the k'-th largest pre-pass tile maximum of row r: k' distinct corpus tokens reach it,
+// so it is a lower bound on the global k'-th value (0 = no bound when fewer than k' tiles were sampled)
 __global__ void __launch_bounds__(S1R_THREADS) stage1_seed_kernel(S1Params p) {
   extern __shared__ __align__(16) uint8_t sd_smem[];
+  __shared__ unsigned int hist[256], bc[2];
   float* sv = reinterpret_cast<float*>(sd_smem);
   const int64_t r = blockIdx.x;
-  const int rb = (int)(r / 128), rl = (int)(r % 128);
-  const int n = p.P * p.kp;
-  int S = 32;
-  while (S < n) S <<= 1;
-  for (int i = threadIdx.x; i < S; i += S1R_THREADS) {
-    float x = -INFINITY;
-    if (i < n) x = p.topv[(((size_t)rb * p.P + i / p.kp) * 128 + rl) * p.kp + i % p.kp];
-    sv[i] = x;
-  }
+  for (int i = threadIdx.x; i < p.NS; i += S1R_THREADS) sv[i] = p.tmax[(size_t)i * p.R + r];
   __syncthreads();
-  block_sort_desc(sv, S);
-  if (threadIdx.x == 0) {
-    const float x = sv[p.kp - 1];
-    p.gthr[r] = x > -INFINITY ? ord_key(x) : 0u;
-  }
+  const float x = p.kp <= p.NS ? block_kth_largest(sv, p.NS, p.kp, hist, bc) : -INFINITY;
+  if (threadIdx.x == 0) p.gthr[r] = x > -INFINITY ? ord_key(x) : 0u;
 }
-
 
 template <typename T>
 __global__ void __launch_bounds__(S1R_THREADS)
@@ -511,12 +534,11 @@ __global__ void __launch_bounds__(S1R_THREADS)
   extern __shared__ __align__(16) uint8_t rf_smem[];
   __shared__ int n_f;
   __shared__ int ovf;
+  __shared__ unsigned int hist[256], bc[2];
   const int64_t r = blockIdx.x;
   const int rb = (int)(r / 128), rl = (int)(r % 128);
   const int n = p.P * p.kp;
-  int S = 32;
-  while (S < n) S <<= 1;
-  float* sv = reinterpret_cast<float*>(rf_smem);                  // [S] (<= 16384)
+  float* sv = reinterpret_cast<float*>(rf_smem);                  // [P * kp] (<= 9472)
   uint64_t* fkey = reinterpret_cast<uint64_t*>(rf_smem);          // reused after the threshold: [S1_FCAP]
   uint32_t* ftok = reinterpret_cast<uint32_t*>(fkey + S1_FCAP);   // [S1_FCAP]
   float* qs = reinterpret_cast<float*>(ftok + S1_FCAP);           // [dim]
@@ -524,23 +546,20 @@ __global__ void __launch_bounds__(S1R_THREADS)
     n_f = 0;
     ovf = 0;
   }
-  for (int i = threadIdx.x; i < S; i += S1R_THREADS) {
-    float x = -INFINITY;
-    if (i < n) {
-      const int it = rb * p.P + i / p.kp;
-      x = p.topv[((size_t)it * 128 + rl) * p.kp + i % p.kp];
-    }
-    sv[i] = x;
+  for (int i = threadIdx.x; i < n; i += S1R_THREADS) {
+    const int it = rb * p.P + i / p.kp;
+    sv[i] = p.topv[((size_t)it * 128 + rl) * p.kp + i % p.kp];
   }
   __syncthreads();
-  block_sort_desc(sv, S);
-  const float thr = sv[p.kp - 1] - 2.0f * p.eps[r];
+  const float thr = block_kth_largest(sv, n, p.kp, hist, bc) - 2.0f * p.eps[r];
   __syncthreads();  // sv is overwritten below
-  for (int pp = 0; pp < p.P; ++pp) {
+  // one item's list per warp lane-strided (lists are short after the pre-pass; items are many)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int pp = warp; pp < p.P; pp += S1R_THREADS / 32) {
     const size_t it = (size_t)rb * p.P + pp;
     const int c = p.cnt[it * 128 + rl];
     const uint2* lst = p.ent + (it * 128 + rl) * p.cap;
-    for (int e = threadIdx.x; e < c; e += S1R_THREADS) {
+    for (int e = lane; e < c; e += 32) {
       const uint2 u = lst[e];
       if (__uint_as_float(u.x) >= thr) {
         const int s = atomicAdd(&n_f, 1);
@@ -598,7 +617,8 @@ __global__ void __launch_bounds__(S1R_THREADS)
 
 struct TcPlan {
   int RB, P, NT, kblocks, stages, items, cap, tile_n;
-  size_t smem, o_eps, o_gthr, o_cnt, o_ent, o_topv, total;
+  int ns_stride, ns;  // threshold pre-pass: tile stride and sampled tiles (0 = no pre-pass)
+  size_t smem, o_eps, o_gthr, o_cnt, o_ent, o_topv, o_tmax, total;
 };
 
 static bool tc_eligible(const cbx_batch* b, int kp) {
@@ -635,6 +655,12 @@ static int plan_tc(const cbx_batch* b, int kp, TcPlan& t) {
   t.cap = std::min(1024, std::max(256, 12 * kp));
   t.o_ent = take(8 * (size_t)t.items * 128 * t.cap);
   t.o_topv = take(4 * (size_t)t.items * 128 * kp);
+  // pre-pass sample: ~16 tiles per SM, at most 4096 tiles and 16 MB of tile maxima
+  int64_t want = std::min<int64_t>({(int64_t)G * 16, 4096, ((int64_t)1 << 22) / std::max<int64_t>(R, 1)});
+  t.ns_stride = want > 0 ? (int)(t.NT / want) : 0;
+  t.ns = t.ns_stride >= 2 ? (t.NT + t.ns_stride - 1) / t.ns_stride : 0;
+  if (t.ns < 4 * kp) t.ns = 0;
+  t.o_tmax = take(4 * (size_t)std::max(t.ns, 1) * R);
   t.total = o;
   return CBX_OK;
 }
@@ -664,6 +690,7 @@ static int run_tc(const cbx_batch* b, int kp, float norm_max, int64_t* nb_tok, d
   p.cnt = reinterpret_cast<int32_t*>(ws + t.o_cnt);
   p.ent = reinterpret_cast<uint2*>(ws + t.o_ent);
   p.topv = reinterpret_cast<float*>(ws + t.o_topv);
+  p.tmax = reinterpret_cast<float*>(ws + t.o_tmax);
   p.status = status;
   CUtensorMap tm_d, tm_q;
   rc = make_tmap(&tm_d, b->d_tokens, b->dtype, b->n_d_tokens, b->dim, (uint32_t)t.tile_n);
@@ -675,21 +702,18 @@ static int run_tc(const cbx_batch* b, int kp, float norm_max, int64_t* nb_tok, d
   CBX_LAUNCH_CHECK("stage1_eps_kernel launch");
   CBX_CUDA_CHECK(cudaFuncSetAttribute(stage1_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
   const int G = sm_count();
-  // threshold pre-pass over every stride-th tile (~16 tiles per CTA): seeds each row's filter with the
-  // k'-th best of a corpus sample, so the main scan appends / inserts almost only true contenders
-  const int stride = t.NT / (G * 16);
-  if (stride >= 2) {
+  // threshold pre-pass over every stride-th tile: seeds each row's filter with the k'-th largest sampled
+  // tile maximum, so the main scan appends / inserts almost only true contenders
+  if (t.ns) {
     S1Params ps = p;
     ps.sample = 1;
-    ps.stride = stride;
-    ps.NS = (t.NT + stride - 1) / stride;
+    ps.stride = t.ns_stride;
+    ps.NS = t.ns;
     ps.P = t.RB >= G ? 1 : std::min(ps.NS, (G + t.RB - 1) / t.RB);
     stage1_scan_kernel<<<std::min(t.RB * ps.P, G), S1_THREADS, t.smem, st>>>(tm_d, tm_q, ps);
     CBX_LAUNCH_CHECK("stage1_scan_kernel (pre-pass) launch");
-    int S = 32;
-    while (S < ps.P * kp) S <<= 1;
-    CBX_CUDA_CHECK(cudaFuncSetAttribute(stage1_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * S));
-    stage1_seed_kernel<<<(unsigned)p.R, S1R_THREADS, 4 * S, st>>>(ps);
+    CBX_CUDA_CHECK(cudaFuncSetAttribute(stage1_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * ps.NS));
+    stage1_seed_kernel<<<(unsigned)p.R, S1R_THREADS, 4 * ps.NS, st>>>(ps);
     CBX_LAUNCH_CHECK("stage1_seed_kernel launch");
   } else {
     CBX_CUDA_CHECK(cudaMemsetAsync(p.gthr, 0, 4 * (size_t)p.R, st));  // key 0: no seed
@@ -699,9 +723,7 @@ static int run_tc(const cbx_batch* b, int kp, float norm_max, int64_t* nb_tok, d
   p.NS = t.NT;
   stage1_scan_kernel<<<std::min(t.items, G), S1_THREADS, t.smem, st>>>(tm_d, tm_q, p);
   CBX_LAUNCH_CHECK("stage1_scan_kernel launch");
-  int S = 32;
-  while (S < t.P * kp) S <<= 1;
-  const size_t rsmem = std::max<size_t>(4 * (size_t)S, 12 * (size_t)S1_FCAP + 4 * (size_t)b->dim);
+  const size_t rsmem = std::max<size_t>(4 * (size_t)t.P * kp, 12 * (size_t)S1_FCAP + 4 * (size_t)b->dim);
   CBX_CUDA_CHECK(cudaFuncSetAttribute(stage1_refine_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
   stage1_refine_kernel<T><<<(unsigned)p.R, S1R_THREADS, rsmem, st>>>(
       static_cast<const T*>(b->q_tokens), static_cast<const T*>(b->d_tokens), p, b->dim, b->clamp_negative, nb_tok,
