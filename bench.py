@@ -321,8 +321,116 @@ def run_ours(args, rank, world, local_rank):
         bandit = run_bandit(args, batch, host_off, cfg, rank, world)
         if rank == 0:
             result["bandit"] = bandit
+    # ------------------------------------------------ Stage 1 (candidate scan) + the reranker facade, cfg4 corpus
+    if not args.no_stage1:
+        del batch
+        torch.cuda.empty_cache()
+        s1 = run_stage1(args, rank, world)
+        if rank == 0:
+            result["stage1"] = s1
     if rank == 0:
         print(json.dumps(result), flush=True)
+
+
+def run_stage1(args, rank, world):
+    """Stage-1 scan (generate_candidates) of one cfg4 query over the 100k-document corpus, then the full
+    ColBanditReranker.rerank through the public API (Stage 1 + ANN bounds + device bandit)."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2602_02827_b200 import _lib
+    from paper_2602_02827_b200 import workloads as W
+    from paper_2602_02827_b200.batch import Corpus, dtype_code
+    from paper_2602_02827_b200.pipeline import stage1_topk
+    from paper_2602_02827_b200.reranker import ColBanditReranker
+
+    cfg = W.CONFIGS["cfg4"]
+    b4, (qo, do, qd) = W.gen_batch_device(cfg, n_queries=1, seed=rank)
+    corpus = Corpus(b4.d_tokens, do, clamp_negative=True)
+    q = b4.q_tokens
+    kp, R, T = 10, int(q.shape[0]), corpus.n_tokens
+    lib = _lib.load()
+    s = _lib.CbxBatch()
+    s.q_tokens, s.n_q_tokens = q.data_ptr(), R
+    s.d_tokens, s.n_d_tokens = corpus.tokens.data_ptr(), T
+    s.dim, s.dtype, s.clamp_negative, s.max_lq = corpus.dim, dtype_code(q.dtype), 1, R
+    wsb = lib.cbx_stage1_workspace_bytes(ctypes.byref(s), kp, _lib.CBX_PATH_TC)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    tok = torch.empty((R, kp), dtype=torch.int64, device="cuda")
+    val = torch.empty((R, kp), dtype=torch.float64, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    norm = corpus.norm_max()
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def call():
+        _lib.check(lib.cbx_stage1_topk(ctypes.byref(s), kp, _lib.CBX_PATH_TC, ctypes.c_float(norm), tok.data_ptr(),
+                                       val.data_ptr(), st.data_ptr(), ws.data_ptr(), wsb, stream), "stage1")
+
+    for _ in range(args.warmup):
+        call()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    tc_status = int(st.item())
+    tok_tc, val_tc = tok.cpu().numpy(), val.cpu().numpy()
+    tok_sx, val_sx = stage1_topk(corpus, q, kp, True, path="simt")
+    hbm_peak, _, peak_kind = _peaks()
+    nbytes = T * corpus.dim * corpus.tokens.element_size()
+    # the facade end to end: host query in, Top-K doc ids out (Stage 1 + pool gather + ANN bounds + bandit)
+    est = ColBanditReranker(k=10, k_prime=kp, similarity="dot", clamp_negative=True).fit(corpus)
+    qh = q.cpu()
+    est.rerank(qh, query_index=0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        o = est.rerank(qh, query_index=0)
+    facade_ms = (time.perf_counter() - t0) * 1e3 / reps
+    if rank != 0:
+        return None
+    out = {"what": "pipeline.generate_candidates Stage-1 scan (cbx_stage1_topk, tcgen05 + float64 refine): one cfg4 "
+                   f"query ({R} tokens) against the 100k-doc cfg4 corpus ({T} tokens, d={corpus.dim}, "
+                   f"{cfg.dtype}), k'={kp}, clamp_negative",
+           "ms": ms, "sims_per_s": R * T / (ms / 1e3),
+           "roofline": {"bound": "hbm", "kernel": "stage1_scan_kernel (+ pre-pass, seed, refine)",
+                        "achieved": nbytes / (ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": nbytes / (ms / 1e3) / 1e9 / hbm_peak, "peak_kind": peak_kind,
+                        "alg_bytes_per_call": nbytes},
+           "parity": {"tc_equals_float64_simt_scan": bool(np.array_equal(tok_tc, tok_sx) and
+                                                          np.array_equal(val_tc, val_sx)),
+                      "tc_status": tc_status},
+           "facade": {"api": "ColBanditReranker(k=10, k_prime=10, similarity='dot').fit(Corpus).rerank(query)",
+                      "ms_per_query": facade_ms, "candidates": len(o.candidates), "coverage": o.coverage,
+                      "terminated_by": o.result.terminated_by},
+           "gpu_launches": 5}
+    if world == 1 and not args.no_cpu:
+        from oracle import stage1_ref
+
+        lim = _blas_one_thread()
+        n_docs = 1500
+        q64 = q.double().cpu().numpy()
+        toks = corpus.tokens[: int(do[n_docs])].double().cpu().numpy()
+        docs = [toks[do[i]:do[i + 1]] for i in range(n_docs)]
+        t0 = time.perf_counter()
+        stage1_ref.generate_candidates(q64, docs, kp, True)
+        cpu_s = time.perf_counter() - t0
+        del lim
+        out["cpu_baseline"] = {"value": R * int(do[n_docs]) / cpu_s, "unit": "similarities/s", "cores": 1,
+                               "kind": "port", "sample": f"oracle/stage1_ref.generate_candidates over the first "
+                                                         f"{n_docs} cfg4 docs ({int(do[n_docs])} tokens), {cpu_s:.1f} s"}
+    return out
 
 
 def run_bandit(args, batch, host_off, cfg, rank, world):
@@ -473,6 +581,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-bandit", action="store_true")
+    ap.add_argument("--no-stage1", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -78,9 +78,23 @@ class ColBanditReranker(BaseEstimator):
 
     # ------------------------------------------------------------------ fit
     def fit(self, X, y=None):
-        """Store the corpus (a list of DocTokens or of (count, dim) arrays) in device memory."""
+        """Store the corpus (a list of DocTokens or of (count, dim) arrays) in device memory.
+
+        A ``batch.Corpus`` (already HBM-resident, e.g. built from one token tensor + offsets) is adopted
+        as is, without a host round trip.
+        """
         from .batch import Corpus
 
+        if isinstance(X, Corpus):
+            if self.bounds_mode not in ("ann", "generic"):
+                raise ValueError(f"bounds_mode must be 'ann' or 'generic', got {self.bounds_mode!r}")
+            if X.doc_ids is None:
+                X.doc_ids = [f"doc{i:04d}" for i in range(X.n_docs)]
+            self.docs_ = X
+            self.dim_ = X.dim
+            self.similarity_ = Similarity(kind=self.similarity, clamp_negative=self.clamp_negative)
+            self.corpus_ = X
+            return self
         if not X:
             raise ValueError("corpus must contain at least one document")
         docs = []
@@ -134,8 +148,7 @@ class ColBanditReranker(BaseEstimator):
             cand = r.candidates
             if self.similarity_.kind == "cosine":  # MaxSimOracle construction (oracle.py:125-131)
                 check_unit_norm(q.vectors, "query vectors")
-                for di in cand.doc_indices:
-                    check_unit_norm(self.docs_[di].vectors, f"doc {self.docs_[di].doc_id!r} vectors")
+                self._check_pool_norms(pool_batch, qi, cand)
             T = q.vectors.shape[0]
             if self.bounds_mode == "ann":
                 bounds = derive_bounds(cand, r.neighbor_lists, self.similarity_)
@@ -166,6 +179,15 @@ class ColBanditReranker(BaseEstimator):
                 result=res,
             ))
         return out
+
+    def _check_pool_norms(self, pool_batch, qi, cand) -> None:
+        qd = pool_batch.host_offsets[2]
+        do = pool_batch.host_offsets[1]
+        a, b = int(do[qd[qi]]), int(do[qd[qi + 1]])
+        rows = pool_batch.d_tokens[a:b].double().cpu().numpy()
+        starts = do[qd[qi]:qd[qi + 1] + 1] - a
+        for j, di in enumerate(cand.doc_indices):
+            check_unit_norm(rows[starts[j]:starts[j + 1]], f"doc {cand.doc_ids[j]!r} vectors")
 
     def _seed_for(self, query_index: int):
         if self.random_state is None:
