@@ -159,6 +159,13 @@ CBX_API int cbx_corpus_rerank_topk(const cbx_batch* b, const int64_t* corpus_off
                                    float* topk_val, int* status, void* workspace, size_t ws_bytes,
                                    void* stream);
 
+/* Static-budget baselines (baselines.py:49-86): sums[i] = exactly rounded
+ * (math.fsum) sum of cells[i * ld + cols[i * cells_per_row + j]] over j, the
+ * partial sums doc_uniform / doc_top_margin rank rows by (baselines.py:38-41).
+ * status[0] |= 1 if an exact-sum expansion overflowed (never for sane data). */
+CBX_API int cbx_row_partial_fsum(const double* cells, int64_t ld, const int32_t* cols, int64_t n_rows,
+                                 int cells_per_row, double* sums, int* status, void* stream);
+
 /* ---------------------------------------------------------------- Stage 1 */
 /* Stage-1 candidate scan, replaces colbandit/pipeline.py:105-158
  * (generate_candidates): for every query-token row r of b->q_tokens (rows of

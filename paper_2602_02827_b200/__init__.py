@@ -3,7 +3,9 @@
 Public surface mirrors the reference package's hot-path entry points:
 
 * ``Similarity``, ``QueryTokens``, ``DocTokens``, ``MaxSimOracle`` (oracle.py)
-* ``BanditConfig``, ``RunResult``, ``run`` (bandit.py); ``full_rerank`` (baselines.py)
+* ``BanditConfig``, ``RunResult``, ``run`` (bandit.py)
+* ``full_rerank``, ``doc_uniform``, ``doc_top_margin`` (baselines.py)
+* ``EvalInstance``, ``sweep_alpha``, ``sweep_budgets``, metrics (evaluation.py; the sweep is one launch)
 * ``RadiusConfig``, ``CellBounds`` (bounds.py)
 * ``generate_candidates``, ``derive_bounds``, ``CandidateSet``, ... (pipeline.py: Stage 1 on the device)
 * ``ColBanditReranker``, ``RerankOutcome`` (reranker.py: the estimator facade)
@@ -16,7 +18,7 @@ plus batched device entry points (``TokenBatch``, ``rerank_topk``,
 __version__ = "0.1.0"
 
 from .bandit import BanditConfig, BanditJob, RunResult, ceil_cells, run, run_batch, select_ambiguous  # noqa: F401
-from .baselines import full_rerank  # noqa: F401
+from .baselines import BudgetConfig, doc_top_margin, doc_uniform, full_rerank  # noqa: F401
 from .batch import TokenBatch, exact_cells, maxsim_scores, rerank_topk, topk  # noqa: F401
 from .bounds import CellBounds, RadiusConfig, fp_correction  # noqa: F401
 from .oracle import DocTokens, MaxSimOracle, QueryTokens, Similarity  # noqa: F401

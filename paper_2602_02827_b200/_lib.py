@@ -106,6 +106,7 @@ SIGNATURES = {
     "cbx_corpus_workspace_bytes": (_SZ, [_I64, _I64, _I64, _I]),
     "cbx_corpus_rerank_topk": (_I, [_P, _P, _I64, _P, _I, _P, _P, _P, _P, _P, _SZ, _P]),
     "cbx_gather_candidates": (_I, [_P, _P, _I64, _I, _I, _P, _I64, _P, _I64, _P, _P, _P]),
+    "cbx_row_partial_fsum": (_I, [_P, _I64, _P, _I64, _I, _P, _P, _P]),
     "cbx_stage1_workspace_bytes": (_SZ, [_P, _I, _I]),
     "cbx_stage1_topk": (_I, [_P, _I, _I, ctypes.c_float, _P, _P, _P, _P, _SZ, _P]),
     "cbx_token_norm_max": (_I, [_P, _I64, _I, _I, _P, _P]),

@@ -53,9 +53,11 @@ def to_torch_tokens(arr, dtype: str | None = None):
     if dtype == "bf16" or (a.dtype == np.uint16 and dtype is None):
         if a.dtype != np.uint16:
             raise ValueError("bf16 tokens must be given as uint16 bit patterns or a torch.bfloat16 tensor")
-        return torch.from_numpy(a.view(np.int16)).view(torch.bfloat16)
+        return torch.from_numpy(a.view(np.int16) if a.flags.writeable else a.view(np.int16).copy()).view(torch.bfloat16)
     if a.dtype not in (np.float16, np.float32, np.float64):
         a = a.astype(np.float64)
+    if not a.flags.writeable:
+        a = a.copy()
     return torch.from_numpy(a)
 
 

@@ -175,3 +175,18 @@ def test_cfg1_bandit_oracle_matches_reference():
     np.testing.assert_array_equal(np.array([(i, t) for i, t, _ in res.reveals]), z["a0_trace_it"])
     np.testing.assert_allclose([v for *_, v in res.reveals], z["a0_trace_v"], rtol=0, atol=1e-15)
     assert res.coverage == z["a0_stats"][0] and res.iterations == z["a0_stats"][1]
+
+
+# ---------------------------------------------------------------- static-budget baselines
+def test_budget_baselines_restatement_matches_reference():
+    from oracle import baselines_ref
+
+    for c in _load_json("budget_small.json"):
+        cells = np.array(c["cells64"])
+        u = baselines_ref.doc_uniform(cells, c["k"], c["gamma"], seed=_seed(c["seed"]))
+        m = baselines_ref.doc_top_margin(cells, np.array(c["lo"]), np.array(c["hi"]), c["k"], c["gamma"])
+        for got, want in ((u, c["uniform"]), (m, c["margin"])):
+            assert got.topk == want["topk"]
+            assert got.coverage == want["coverage"]
+            assert [list(x) for x in got.reveals] == want["reveals"]
+            assert got.terminated_by == want["terminated_by"] == "budget"
