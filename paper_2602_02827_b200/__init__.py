@@ -5,6 +5,7 @@ Public surface mirrors the reference package's hot-path entry points:
 * ``Similarity``, ``QueryTokens``, ``DocTokens``, ``MaxSimOracle`` (oracle.py)
 * ``BanditConfig``, ``RunResult``, ``run`` (bandit.py)
 * ``full_rerank``, ``doc_uniform``, ``doc_top_margin`` (baselines.py)
+* ``io``: CBM1 / CBH1 / manifest formats with loaders straight into HBM
 * ``EvalInstance``, ``sweep_alpha``, ``sweep_budgets``, metrics (evaluation.py; the sweep is one launch)
 * ``RadiusConfig``, ``CellBounds`` (bounds.py)
 * ``generate_candidates``, ``derive_bounds``, ``CandidateSet``, ... (pipeline.py: Stage 1 on the device)
@@ -21,7 +22,7 @@ from .bandit import BanditConfig, BanditJob, RunResult, ceil_cells, run, run_bat
 from .baselines import BudgetConfig, doc_top_margin, doc_uniform, full_rerank  # noqa: F401
 from .batch import TokenBatch, exact_cells, maxsim_scores, rerank_topk, topk  # noqa: F401
 from .bounds import CellBounds, RadiusConfig, fp_correction  # noqa: F401
-from .oracle import DocTokens, MaxSimOracle, QueryTokens, Similarity  # noqa: F401
+from .oracle import DocTokens, MaxSimOracle, ObservationLedger, QueryTokens, RowStats, Similarity, reveal  # noqa: F401
 from .pipeline import (CandidateSet, TokenNeighbor, TokenNeighborList, derive_bounds,  # noqa: F401
                        generate_candidates, load_candidates, save_candidates)
 from .reranker import ColBanditReranker, RerankOutcome  # noqa: F401
