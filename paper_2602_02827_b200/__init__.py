@@ -21,8 +21,10 @@ __version__ = "0.1.0"
 from .bandit import BanditConfig, BanditJob, RunResult, ceil_cells, run, run_batch, select_ambiguous  # noqa: F401
 from .baselines import BudgetConfig, doc_top_margin, doc_uniform, full_rerank  # noqa: F401
 from .batch import TokenBatch, exact_cells, maxsim_scores, rerank_topk, topk  # noqa: F401
-from .bounds import CellBounds, RadiusConfig, fp_correction  # noqa: F401
-from .oracle import DocTokens, MaxSimOracle, ObservationLedger, QueryTokens, RowStats, Similarity, reveal  # noqa: F401
+from .bounds import (CellBounds, DecisionState, RadiusConfig, RowStats, compute_decision_state,  # noqa: F401
+                     decision_interval, effective_radius, empirical_std, estimated_score, fp_correction, hard_bounds,
+                     score_proxy)
+from .oracle import DocTokens, MaxSimOracle, ObservationLedger, QueryTokens, Similarity, reveal  # noqa: F401
 from .pipeline import (CandidateSet, TokenNeighbor, TokenNeighborList, derive_bounds,  # noqa: F401
                        generate_candidates, load_candidates, save_candidates)
 from .reranker import ColBanditReranker, RerankOutcome  # noqa: F401

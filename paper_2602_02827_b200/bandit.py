@@ -27,7 +27,7 @@ from . import _lib
 from .bounds import CellBounds, RadiusConfig
 
 __all__ = ["BanditConfig", "RunResult", "EXPLORE_MODES", "run", "run_batch", "ceil_cells", "select_ambiguous",
-           "BanditJob"]
+           "select_token", "static_warmup", "init_one_per_row", "BanditJob"]
 
 EXPLORE_MODES = ("epsilon-greedy", "static-warmup", "uniform-row")
 _MODE_CODE = {"epsilon-greedy": _lib.CBX_EPSILON_GREEDY, "static-warmup": _lib.CBX_STATIC_WARMUP,
@@ -88,6 +88,44 @@ def ceil_cells(fraction: float, total: int) -> int:
 
 def select_ambiguous(i_plus: int, i_minus: int, width_plus: float, width_minus: float) -> int:
     return i_plus if width_plus >= width_minus else i_minus
+
+
+def select_token(ledger, bounds: CellBounds, i: int, epsilon: float, rng: np.random.Generator) -> int:
+    """bandit.py:116-136 — an unrevealed column of row i: uniform with probability epsilon (the draw is
+    always made), else the widest support, ties to the lowest column. Host helper for ledger-driven callers;
+    the device loop makes the same choice in cbx_bandit_run."""
+    cols = ledger.unobserved_cols(i)
+    if not cols:
+        raise ValueError(f"row {i} is fully revealed; no column to select")
+    if rng.random() < epsilon:
+        return cols[int(rng.integers(len(cols)))]
+    widths = bounds.hi[i, cols] - bounds.lo[i, cols]
+    return cols[int(np.argmax(widths))]
+
+
+def static_warmup(oracle, ledger, gamma_init: float, rng: np.random.Generator):
+    """bandit.py:139-156 — reveal ceil(gamma_init * N * T) cells uniformly without replacement."""
+    from .oracle import reveal
+
+    if not 0.0 <= gamma_init <= 1.0:
+        raise ValueError(f"gamma_init must be in [0, 1], got {gamma_init}")
+    total = ledger.n_rows * ledger.n_cols
+    m = ceil_cells(gamma_init, total)
+    if m == 0:
+        return ledger
+    for f in rng.choice(total, size=m, replace=False):
+        i, t = divmod(int(f), ledger.n_cols)
+        reveal(ledger, oracle, i, t)
+    return ledger
+
+
+def init_one_per_row(oracle, ledger, rng: np.random.Generator):
+    """bandit.py:159-166 — one uniformly random cell per row (the epsilon-greedy warm start)."""
+    from .oracle import reveal
+
+    for i in range(ledger.n_rows):
+        reveal(ledger, oracle, i, int(rng.integers(ledger.n_cols)))
+    return ledger
 
 
 @dataclass

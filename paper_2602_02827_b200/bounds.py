@@ -1,12 +1,14 @@
-"""Bound configuration objects of the reference, mirrored for the drop-in API.
+"""Bound configuration objects and interval scalars of the reference, mirrored for the drop-in API.
 
 ``RadiusConfig`` / ``CellBounds`` keep the reference's field names, defaults,
 validation and messages (colbandit/bounds.py:112-191). The interval
-arithmetic itself (hard bounds, radius, decision interval, score proxy —
+arithmetic of the loop (hard bounds, radius, decision interval, score proxy —
 bounds.py:72-263) runs inside the bandit kernel (csrc/bandit.cu
-``row_interval``); only ``log_term`` is evaluated here, on the host, with
-``math.log`` exactly as the reference does (bounds.py:138-143), because a
-device ``log`` may differ in the last ulp.
+``row_interval``); the scalar functions below are the same arithmetic on the
+host for callers that drive their own ledger (``oracle.ObservationLedger``).
+``log_term`` is always evaluated here with ``math.log`` exactly as the
+reference does (bounds.py:138-143), because a device ``log`` may differ in
+the last ulp.
 """
 
 from __future__ import annotations
@@ -18,7 +20,9 @@ import numpy as np
 
 UNION_MODES = ("per-document", "per-document-and-size")
 
-__all__ = ["RadiusConfig", "CellBounds", "UNION_MODES", "fp_correction"]
+__all__ = ["RadiusConfig", "CellBounds", "UNION_MODES", "fp_correction", "RowStats", "empirical_std",
+           "estimated_score", "effective_radius", "hard_bounds", "decision_interval", "DecisionState",
+           "compute_decision_state", "score_proxy"]
 
 
 @dataclass(frozen=True)
@@ -99,3 +103,100 @@ class CellBounds:
             else:
                 self._uniform = False
         return self._uniform or None
+
+
+# ---------------------------------------------------------------- interval scalars (bounds.py:45-263)
+@dataclass(frozen=True)
+class RowStats:
+    """Revealed-cell statistics of one row: count, exact (fsum) total, Welford mean and m2."""
+
+    n: int
+    total: float
+    mean: float
+    m2: float
+
+    @classmethod
+    def from_values(cls, values) -> "RowStats":
+        """Two-pass construction (bounds.py:59-69)."""
+        vals = [float(v) for v in values]
+        n = len(vals)
+        if n == 0:
+            return cls(0, 0.0, 0.0, 0.0)
+        total = math.fsum(vals)
+        mean = total / n
+        return cls(n, total, mean, math.fsum((v - mean) ** 2 for v in vals))
+
+
+def empirical_std(stats: RowStats) -> float:
+    """bounds.py:72-80 — unbiased sample std; undefined below two observations."""
+    if stats.n <= 1:
+        raise ValueError(f"empirical_std undefined for n={stats.n}; need at least 2 observations")
+    return math.sqrt(max(stats.m2, 0.0) / (stats.n - 1))
+
+
+def estimated_score(stats: RowStats, n_cols: int) -> float:
+    """bounds.py:83-94 — T * (total / n); the exact total at full reveal."""
+    if stats.n == 0:
+        raise ValueError("estimated score undefined for an unobserved row")
+    if stats.n == n_cols:
+        return stats.total
+    return n_cols * (stats.total / stats.n)
+
+
+def effective_radius(stats: RowStats, n_cols: int, cfg: RadiusConfig, n_rows: int) -> float:
+    """bounds.py:146-158 — alpha * T * sigma * sqrt(2 log_term / n) * sqrt(rho_n); inf for n <= 1."""
+    if stats.n <= 1:
+        return math.inf
+    sigma = empirical_std(stats)
+    rho = fp_correction(stats.n, n_cols)
+    return cfg.alpha_ef * n_cols * sigma * math.sqrt(2.0 * cfg.log_term(n_rows, n_cols) / stats.n) * math.sqrt(rho)
+
+
+def hard_bounds(ledger, bounds: CellBounds, i: int) -> tuple[float, float]:
+    """bounds.py:194-208 — revealed values plus unrevealed support bounds, exactly rounded sums."""
+    if (ledger.n_rows, ledger.n_cols) != (bounds.n_rows, bounds.n_cols):
+        raise ValueError("ledger and bounds shapes differ")
+    observed = math.fsum(ledger.row_values(i))
+    rest = ledger.unobserved_cols(i)
+    return (observed + math.fsum(float(bounds.lo[i, t]) for t in rest),
+            observed + math.fsum(float(bounds.hi[i, t]) for t in rest))
+
+
+def decision_interval(est_score, radius: float, hard_lo: float, hard_hi: float) -> tuple[float, float]:
+    """bounds.py:211-225 — the statistical interval clipped into the hard envelope (both ends)."""
+    if est_score is None or math.isinf(radius):
+        return hard_lo, hard_hi
+    return min(max(hard_lo, est_score - radius), hard_hi), max(min(hard_hi, est_score + radius), hard_lo)
+
+
+@dataclass(frozen=True)
+class DecisionState:
+    """bounds.py:228-241."""
+
+    est_score: float | None
+    hard_lo: float
+    hard_hi: float
+    radius: float
+    lcb: float
+    ucb: float
+
+    @property
+    def width(self) -> float:
+        return self.ucb - self.lcb
+
+
+def compute_decision_state(ledger, bounds: CellBounds, i: int, radius_cfg: RadiusConfig) -> DecisionState:
+    """bounds.py:244-256."""
+    stats = ledger.row_stats(i)
+    h_lo, h_hi = hard_bounds(ledger, bounds, i)
+    est = None if stats.n == 0 else estimated_score(stats, ledger.n_cols)
+    radius = effective_radius(stats, ledger.n_cols, radius_cfg, ledger.n_rows)
+    lcb, ucb = decision_interval(est, radius, h_lo, h_hi)
+    return DecisionState(est, h_lo, h_hi, radius, lcb, ucb)
+
+
+def score_proxy(state: DecisionState) -> float:
+    """bounds.py:259-263 — the estimate, or the hard midpoint before any reveal."""
+    if state.est_score is None:
+        return 0.5 * (state.hard_lo + state.hard_hi)
+    return state.est_score
