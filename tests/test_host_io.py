@@ -78,7 +78,7 @@ def test_ledger_and_reveal_semantics():
     assert led.coverage() == 0.5 and led.observed_count == 3 and o.charged == 3
     assert led.observed_cols(0) == [0, 2] and led.unobserved_cols(0) == [1] and led.row_values(0) == [1.0, 0.5]
     st = led.row_stats(0)
-    assert (st.count, st.total, st.mean, st.m2) == (2, 1.5, 0.75, 0.125)
+    assert (st.n, st.total, st.mean, st.m2) == (2, 1.5, 0.75, 0.125)
     with pytest.raises(ValueError, match="already revealed"):
         reveal(led, o, 0, 2)
     with pytest.raises(IndexError, match="column"):
