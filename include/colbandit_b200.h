@@ -256,9 +256,10 @@ CBX_API int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_
                            int32_t* trace_i, int32_t* trace_t, double* trace_v,
                            cbx_bandit_out* out, void* stream);
 
-/* Profiling hook: when set (device pointer to n_runs * 8 uint64), every
+/* Profiling hook: when set (device pointer to n_runs * 16 uint64), every
  * following cbx_bandit_run writes per-run SM-cycle counters of its phases
- * [scan, decide, reveal, update, warm-up, total]; NULL disables. */
+ * [scan, decide, reveal, trees, warm-up, total, row update, sync, and the
+ * row update's sub-phases setup, Welford, exact sum, interval]; NULL disables. */
 CBX_API void cbx_bandit_set_profile(void* counters);
 
 #ifdef __cplusplus

@@ -202,18 +202,19 @@ constexpr uint32_t TIE_EMPTY = 0xFFFFFFFFu;
 // summarises level l-1 nodes [32g, 32g + 32); the single top node is the
 // answer. A changed row costs one warp pass per level (32-wide redux), so a
 // reveal is O(log32 N) instead of a scan of the pool.
+// Level sizes and offsets are recomputed on the fly (ceil(size / 32) per level)
+// so nothing here is an indexed local array: the walk stays in registers.
 struct Trees {
   uint64_t* key;   // [4][nn]
   uint32_t* tie;   // [4][nn]
-  int nn, nlev;
-  int off[8], size[8];
+  int nn, nlev, size0, root_off;
   __device__ void carve(uint8_t* base, int N) {
     nlev = 0;
     nn = 0;
-    int sz = (N + 31) / 32;
+    size0 = (N + 31) / 32;
+    int sz = size0;
     while (true) {
-      off[nlev] = nn;
-      size[nlev] = sz;
+      root_off = nn;
       nn += sz;
       ++nlev;
       if (sz == 1 || nlev == 8) break;
@@ -223,7 +224,7 @@ struct Trees {
     tie = reinterpret_cast<uint32_t*>(key + 4 * nn);
   }
   __device__ __forceinline__ Cand root(int s) const {
-    const int r = s * nn + off[nlev - 1];
+    const int r = s * nn + root_off;
     return Cand{key[r], tie[r]};
   }
 };
@@ -232,21 +233,20 @@ struct Trees {
 __device__ __forceinline__ void tree_leaf(const Trees& t, const RowsView& rv, int N, int g, int lane,
                                           unsigned mask = 0xFu) {
   const int i = g * 32 + lane;
-  Cand c[4] = {{0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}};
-  if (i < N) {
-    const uint64_t pk = ord_key(rv.proxy[i]);
-    if (rv.member[i]) {
-      c[0] = Cand{~ord_key(rv.lcb[i]), (uint32_t)i};
-      c[3] = Cand{~pk, ~(uint32_t)i};
-    } else {
-      c[1] = Cand{ord_key(rv.ucb[i]), (uint32_t)i};
-      c[2] = Cand{pk, (uint32_t)i};
-    }
-  }
+  const bool live = i < N;
+  const bool mem = live && rv.member[i];
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     if (!(mask >> s & 1u)) continue;
-    const Cand w = warp_best(c[s]);
+    // selections 0 and 3 range over members, 1 and 2 over non-members (no indexed local array)
+    Cand c{0, TIE_EMPTY};
+    if (live && (mem == (s == 0 || s == 3))) {
+      if (s == 0) c = Cand{~ord_key(rv.lcb[i]), (uint32_t)i};
+      else if (s == 1) c = Cand{ord_key(rv.ucb[i]), (uint32_t)i};
+      else if (s == 2) c = Cand{ord_key(rv.proxy[i]), (uint32_t)i};
+      else c = Cand{~ord_key(rv.proxy[i]), ~(uint32_t)i};
+    }
+    const Cand w = warp_best(c);
     if (lane == 0) {
       t.key[s * t.nn + g] = w.key;
       t.tie[s * t.nn + g] = w.tie;
@@ -254,22 +254,23 @@ __device__ __forceinline__ void tree_leaf(const Trees& t, const RowsView& rv, in
   }
 }
 
-// warp-collective: level-l node g from its children at level l-1
-__device__ __forceinline__ void tree_node(const Trees& t, int l, int g, int lane, unsigned mask = 0xFu) {
+// warp-collective: node g of a level at offset `off` from its children (level at `coff`, `csize` nodes)
+__device__ __forceinline__ void tree_node(const Trees& t, int coff, int csize, int off, int g, int lane,
+                                          unsigned mask = 0xFu) {
   const int c0 = g * 32 + lane;
-  const bool ok = c0 < t.size[l - 1];
+  const bool ok = c0 < csize;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     if (!(mask >> s & 1u)) continue;
     Cand c{0, TIE_EMPTY};
     if (ok) {
-      const int idx = s * t.nn + t.off[l - 1] + c0;
+      const int idx = s * t.nn + coff + c0;
       c = Cand{t.key[idx], t.tie[idx]};
     }
     const Cand w = warp_best(c);
     if (lane == 0) {
-      t.key[s * t.nn + t.off[l] + g] = w.key;
-      t.tie[s * t.nn + t.off[l] + g] = w.tie;
+      t.key[s * t.nn + off + g] = w.key;
+      t.tie[s * t.nn + off + g] = w.tie;
     }
   }
 }
@@ -279,10 +280,14 @@ __device__ __forceinline__ void tree_update_row(const Trees& t, const RowsView& 
                                                 unsigned mask) {
   int g = i / 32;
   tree_leaf(t, rv, N, g, lane, mask);
+  int coff = 0, csize = t.size0;
   for (int l = 1; l < t.nlev; ++l) {
     __syncwarp();
     g /= 32;
-    tree_node(t, l, g, lane, mask);
+    const int off = coff + csize;
+    tree_node(t, coff, csize, off, g, lane, mask);
+    coff = off;
+    csize = (csize + 31) / 32;
   }
   __syncwarp();
 }
@@ -441,6 +446,193 @@ __device__ __forceinline__ double tokens_max_dot(const T* __restrict__ dtok, int
   return best;
 }
 
+// 16-bit inputs: the same maximum, found by an fp32 interval screen so that
+// the conversion (F2F.F64, 16 lanes per clock per SM) and float64 shuffle
+// work of the MIO pipe — which bound the all-float64 scan above — is spent
+// on one or two rows per warp instead of every row.
+//  * Layout: SG lanes per token row, each owning SV = 4 16-byte vectors
+//    (sub, sub + SG, ...): log2(SG) fp32 butterfly levels per row (SG = 4 for
+//    d = 128 16-bit tokens, against 4 float64 levels in tokens_max_dot).
+//  * Interval: a product of two fp16 (11-bit) or bf16 (8-bit) significands is
+//    exact in fp32, so the fp32 dot s of a row is within
+//    gamma_36 * sum|x_k q_k| <= 2^-18.8 |x| |q| of its float64 value
+//    (Cauchy-Schwarz; <= 36 roundings per lane chain + butterfly). With
+//    eps = 2^-16 |x| |q| + 2^-40 (|x|^2, |q|^2 accumulated in fp32; 2^-40
+//    absorbs bf16 products and squares that underflow) the row's value lies
+//    in [lb, ub] = [s - eps, s + eps], rounded outwards. Queries with |q|^2
+//    outside [2^-60, 2^60] are not screened (every row is exact).
+//  * Prune: LB = max(clamp floor, best exact value, every lb seen) is a lower
+//    bound on the answer, so a row with ub < LB cannot be (or tie) the
+//    maximum. Rows with ub >= LB wait in a per-warp list (entry k in lane k)
+//    and are recomputed in float64 by the whole warp — highest ub first, one
+//    16-byte vector per lane, fma chain + butterfly — when the list fills or
+//    the range ends; each exact value raises LB and prunes the rest. NaN or
+//    overflowed intervals are never pruned and never raise LB.
+// The result is the exact maximum of the float64 dots, as in tokens_max_dot.
+__device__ __forceinline__ uint32_t ord_key_f(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+template <typename T, int SG, int B>
+__device__ __forceinline__ double tokens_max_screen(const T* __restrict__ dtok, int64_t j0, int64_t j1,
+                                                    const T* __restrict__ q, int dim, int wid, int nwarps, int lane,
+                                                    double best, const unsigned long long* shared_best) {
+  constexpr int SV = 4;
+  constexpr int RPW = 32 / SG;
+  constexpr int EV = (SG * SV + 31) / 32;
+  const int nvec = dim / 8;
+  const int sub = lane % SG, grp = lane / SG;
+  float qf[SV][8];
+  float nq2 = 0.0f;
+#pragma unroll
+  for (int u = 0; u < SV; ++u) {
+    const int v = sub + u * SG;
+    uint4 w = make_uint4(0, 0, 0, 0);
+    if (v < nvec) w = __ldg(reinterpret_cast<const uint4*>(q) + v);
+    const T* x = reinterpret_cast<const T*>(&w);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      qf[u][k] = Elem<T>::to_f(x[k]);
+      nq2 = __fmaf_rn(qf[u][k], qf[u][k], nq2);
+    }
+  }
+#pragma unroll
+  for (int o = SG / 2; o > 0; o >>= 1) nq2 = __fadd_rn(nq2, __shfl_xor_sync(0xffffffffu, nq2, o));
+  const bool screen = nq2 >= 0x1p-60f && nq2 <= 0x1p60f;
+  const float qn = __fsqrt_ru(nq2);
+  float LB = best == -INFINITY ? -INFINITY : __double2float_rd(best);
+  float p_ub = -INFINITY;  // pending list: entry `lane`
+  int64_t p_j = 0;
+  int pc = 0;
+
+  // exact float64 value of pending rows, highest ub first, until none can reach LB
+  auto flush = [&]() {
+    while (true) {
+      const uint32_t key = (lane < pc && !(p_ub < LB)) ? ord_key_f(p_ub) | 1u : 0u;  // NaN ub: ord_key_f > 0
+      const uint32_t kmax = __reduce_max_sync(0xffffffffu, key);
+      if (kmax == 0u) break;
+      const int L = __ffs(__ballot_sync(0xffffffffu, key == kmax)) - 1;
+      const int64_t j = __shfl_sync(0xffffffffu, p_j, L);
+      if (lane == L) p_ub = -INFINITY;
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < EV; ++e) {
+        const int v = lane + 32 * e;
+        if (v < nvec) {
+          const uint4 w = __ldg(reinterpret_cast<const uint4*>(dtok + j * dim) + v);
+          const uint4 qw = __ldg(reinterpret_cast<const uint4*>(q) + v);
+          const T* x = reinterpret_cast<const T*>(&w);
+          const T* y = reinterpret_cast<const T*>(&qw);
+          double part = 0.0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) part = fma(Elem<T>::to_d(x[k]), Elem<T>::to_d(y[k]), part);
+          acc += part;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (acc > best) {
+        best = acc;
+        LB = fmaxf(LB, __double2float_rd(acc));
+      }
+    }
+    pc = 0;
+  };
+
+  const int64_t ngroups = (int64_t)nwarps * RPW;
+  for (int64_t jw = j0 + (int64_t)wid * RPW; jw < j1; jw += ngroups * B) {  // warp-uniform
+    uint4 buf[B][SV];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int64_t j = jw + grp + (int64_t)b * ngroups;
+#pragma unroll
+      for (int u = 0; u < SV; ++u) {
+        const int v = sub + u * SG;
+        if (j < j1 && v < nvec) buf[b][u] = __ldg(reinterpret_cast<const uint4*>(dtok + j * dim) + v);
+        else buf[b][u] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    float ub[B];
+    float lbmax = -INFINITY;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      float s = 0.0f, n2 = 0.0f;
+#pragma unroll
+      for (int u = 0; u < SV; ++u) {
+        const T* x = reinterpret_cast<const T*>(&buf[b][u]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float xf = Elem<T>::to_f(x[k]);
+          s = __fmaf_rn(xf, qf[u][k], s);
+          n2 = __fmaf_rn(xf, xf, n2);
+        }
+      }
+#pragma unroll
+      for (int o = SG / 2; o > 0; o >>= 1) {
+        s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+        n2 = __fadd_rn(n2, __shfl_xor_sync(0xffffffffu, n2, o));
+      }
+      const int64_t j = jw + grp + (int64_t)b * ngroups;
+      const float eps = __fmaf_ru(__fmul_ru(__fsqrt_ru(n2), qn), 0x1p-16f, 0x1p-40f);
+      const bool live = j < j1;
+      ub[b] = !live ? -INFINITY : (screen ? __fadd_ru(s, eps) : INFINITY);
+      const float lb = __fsub_rd(s, eps);
+      if (live && screen && lb <= 3.0e38f && lb >= -3.0e38f) lbmax = fmaxf(lbmax, lb);  // finite only
+    }
+    if (shared_best) {
+      const double sb = ord_val(*reinterpret_cast<const volatile unsigned long long*>(shared_best));
+      if (sb > best) best = sb;
+    }
+    // LB over the warp: the largest finite lb of this step (ordered-key max), the best exact value
+    const uint32_t lk = __reduce_max_sync(0xffffffffu, lbmax == -INFINITY ? 0u : ord_key_f(lbmax));
+    if (lk) LB = fmaxf(LB, __uint_as_float((lk & 0x80000000u) ? (lk & 0x7FFFFFFFu) : ~lk));
+    if (best != -INFINITY) LB = fmaxf(LB, __double2float_rd(best));
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      unsigned m = __ballot_sync(0xffffffffu, sub == 0 && !(ub[b] < LB));
+      while (m) {  // warp-uniform: append the row of group leader L to the pending list
+        const int L = __ffs(m) - 1;
+        m &= m - 1;
+        const float u = __shfl_sync(0xffffffffu, ub[b], L);
+        if (lane == pc) {
+          p_ub = u;
+          p_j = jw + L / SG + (int64_t)b * ngroups;
+        }
+        if (++pc == 32) flush();
+      }
+    }
+  }
+  if (shared_best) {
+    const double sb = ord_val(*reinterpret_cast<const volatile unsigned long long*>(shared_best));
+    if (sb > best) {
+      best = sb;
+      LB = fmaxf(LB, __double2float_rd(sb));
+    }
+  }
+  flush();
+  return best;
+}
+
+#ifndef CBX_BD_SCREEN
+#define CBX_BD_SCREEN 1
+#endif
+#ifndef CBX_BD_SCREEN_B
+#define CBX_BD_SCREEN_B 2  // rows per lane group in flight
+#endif
+// maximum over tokens [j0, j1) of the float64 dot with q; `init` is the clamp floor.
+// (G, VPL) is the all-float64 layout; wid/nwarps/lane place the calling warp for the screened layout.
+template <typename T, int G, int VPL, int B>
+__device__ __forceinline__ double tokens_max(const T* __restrict__ dtok, int64_t j0, int64_t j1, const T* q, int dim,
+                                             int gid, int ngroups, int sub, double init, int wid, int nwarps,
+                                             const unsigned long long* shared_best) {
+  if constexpr (sizeof(T) == 2 && CBX_BD_SCREEN) {
+    constexpr int SG = (G * VPL) / 4 < 1 ? 1 : (G * VPL) / 4;
+    return tokens_max_screen<T, SG, CBX_BD_SCREEN_B>(dtok, j0, j1, q, dim, wid, nwarps, threadIdx.x & 31, init, shared_best);
+  } else {
+    return tokens_max_dot<T, G, VPL, B>(dtok, j0, j1, q, dim, gid, ngroups, sub, init);
+  }
+}
+
 // ----------------------------------------------------------------- the kernel
 template <typename T, int G, int VPL>
 __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParams P) {
@@ -470,6 +662,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
     int pad;
     unsigned long long cellkey;
     int32_t swap_in, swap_out;  // best non-member / worst member of the last selection
+    int32_t partner;            // row whose membership swapped with i* this iteration (-1: none)
   };
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(bd_smem);
   Cand* red = reinterpret_cast<Cand*>(bd_smem + 128);                 // [4][BD_WARPS]
@@ -499,6 +692,17 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
   }
   const double init_cell = P.clamp_negative ? 0.0 : -INFINITY;
 
+  // optional phase cycle counters (thread 0; cbx_bandit_set_profile)
+  unsigned long long ph[16] = {0};
+  unsigned long long tc0 = clock64();
+#define BD_PHASE(k)                            \
+  do {                                         \
+    if (P.prof && tid == 0) {                  \
+      const unsigned long long _n = clock64(); \
+      ph[k] += _n - tc0;                       \
+      tc0 = _n;                                \
+    }                                          \
+  } while (0)
   // exact sum of a row's revealed values, rounded like math.fsum
   auto obs_sum = [&](int i) -> double {
     if (rv.exp_mode[i]) return exp_value(&g_obs[i]);
@@ -523,11 +727,14 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
   auto reveal_update = [&](int i, int t, double v) -> bool {
     const int n = rv.cnt[i] + 1;
     double mean = rv.mean[i], m2 = rv.m2[i];
+    BD_PHASE(8);
     const double d = __dsub_rn(v, mean);
     mean = __dadd_rn(mean, __ddiv_rn(d, (double)n));
     m2 = __dadd_rn(m2, __dmul_rn(d, __dsub_rn(v, mean)));
+    BD_PHASE(9);
     bool ok = obs_add(i, v);
     const double obs = obs_sum(i);
+    BD_PHASE(10);
     rv.mean[i] = mean;
     rv.m2[i] = m2;
     rv.unrev[i] &= ~(1ull << t);
@@ -546,14 +753,16 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
     rv.proxy[i] = px;
     rv.lcb[i] = l;
     rv.ucb[i] = u;
+    BD_PHASE(11);
     return ok;
   };
 
   // H[i, t] by one warp (warm-up cells)
   auto cell_warp = [&](int i, int t) -> double {
     if (!tokens) return P.matrix[(R.row_begin + i) * P.ld_matrix + t];
-    double best = tokens_max_dot<T, GW, VPL, (VPL == 1 ? 8 : 4)>(dtok, dto[i], dto[i + 1], qtok + (int64_t)t * dim,
-                                                                   dim, lane / GW, 32 / GW, lane % GW, init_cell);
+    double best = tokens_max<T, GW, VPL, (VPL == 1 ? 8 : 4)>(dtok, dto[i], dto[i + 1], qtok + (int64_t)t * dim,
+                                                                   dim, lane / GW, 32 / GW, lane % GW, init_cell, 0, 1,
+                                                                   nullptr);
 #pragma unroll
     for (int o = 16; o >= GW; o >>= 1) {
       const double w = __shfl_xor_sync(0xffffffffu, best, o);
@@ -581,10 +790,17 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       __syncthreads();
     }
     if (use_tree) {
+      int coff = 0, csize = tr.size0;
       for (int l = 0; l < tr.nlev; ++l) {
-        for (int g = warp; g < tr.size[l]; g += BD_WARPS) {
+        const int off = l == 0 ? 0 : coff + csize;
+        const int size = l == 0 ? tr.size0 : (csize + 31) / 32;
+        for (int g = warp; g < size; g += BD_WARPS) {
           if (l == 0) tree_leaf(tr, rv, N, g, lane);
-          else tree_node(tr, l, g, lane);
+          else tree_node(tr, coff, csize, off, g, lane);
+        }
+        if (l > 0) {
+          coff = off;
+          csize = size;
         }
         __syncthreads();
       }
@@ -647,16 +863,8 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
   const double eps = R.explore_mode == CBX_UNIFORM_ROW ? 1.0 : R.epsilon;
   const int64_t total_cells = (int64_t)N * TC;
   int term = CBX_TERM_SEPARATION;
-  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
-  unsigned long long tc0 = clock64(), tcs = tc0;
-#define BD_PHASE(k)                            \
-  do {                                         \
-    if (P.prof && tid == 0) {                  \
-      const unsigned long long _n = clock64(); \
-      ph[k] += _n - tc0;                       \
-      tc0 = _n;                                \
-    }                                          \
-  } while (0)
+  tc0 = clock64();
+  const unsigned long long tcs = tc0;
 
   while (true) {
     BD_PHASE(3);
@@ -814,8 +1022,8 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
     // ---------------------------------------------------------- reveal one cell
     const int i_star = ctrl->i_star, t_star = ctrl->t_star;
     if (tokens) {
-      double best = tokens_max_dot<T, G, VPL, B>(dtok, dto[i_star], dto[i_star + 1], qtok + (int64_t)t_star * dim, dim,
-                                                 gid, NGROUPS, sub, init_cell);
+      double best = tokens_max<T, G, VPL, B>(dtok, dto[i_star], dto[i_star + 1], qtok + (int64_t)t_star * dim, dim,
+                                             gid, NGROUPS, sub, init_cell, warp, BD_WARPS, &ctrl->cellkey);
 #pragma unroll
       for (int o = 16; o >= G; o >>= 1) {
         const double w = __shfl_xor_sync(0xffffffffu, best, o);
@@ -858,15 +1066,34 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
         }
       }
     }
+#ifndef CBX_BD_TREE_PAR
+#define CBX_BD_TREE_PAR 1
+#endif
+#if CBX_BD_TREE_PAR
+    if (use_tree) {
+      if (tid == 0) ctrl->partner = partner;
+      BD_PHASE(6);
+      __syncthreads();
+      BD_PHASE(7);
+      // a member lives in trees 0 (i+) and 3 (worst), a non-member in 1 (i-) and 2 (best non-member);
+      // a membership swap touches all four for both rows. Warp s refreshes tree s.
+      partner = ctrl->partner;
+      const unsigned mask = partner >= 0 ? 0xFu : (rv.member[i_star] ? 0x9u : 0x6u);
+      if (warp < 4 && (mask >> warp & 1u)) {
+        tree_update_row(tr, rv, N, i_star, lane, 1u << warp);
+        if (partner >= 0) tree_update_row(tr, rv, N, partner, lane, 1u << warp);
+      }
+    }
+#else
+    BD_PHASE(6);
     if (use_tree && warp == 0) {
       __syncwarp();
       partner = __shfl_sync(0xffffffffu, partner, 0);
-      // a member lives in trees 0 (i+) and 3 (worst), a non-member in 1 (i-) and 2 (best non-member);
-      // a membership swap touches all four for both rows
       const unsigned mask = partner >= 0 ? 0xFu : (rv.member[i_star] ? 0x9u : 0x6u);
       tree_update_row(tr, rv, N, i_star, lane, mask);
       if (partner >= 0) tree_update_row(tr, rv, N, partner, lane, 0xFu);
     }
+#endif
     __syncthreads();
   }
 
@@ -896,7 +1123,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
     P.out[blockIdx.x] = o;
     if (P.prof) {
       ph[5] = clock64() - tcs;
-      for (int k = 0; k < 6; ++k) P.prof[blockIdx.x * 8 + k] = ph[k];
+      for (int k = 0; k < 16; ++k) P.prof[blockIdx.x * 16 + k] = ph[k];
     }
   }
 #undef BD_PHASE

@@ -19,12 +19,14 @@ ap.add_argument("--queries", type=int, default=None)
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--phases", action="store_true")
 ap.add_argument("--selection", default="auto")
+ap.add_argument("--runs", type=int, default=None, help="runs over the first --queries queries, round robin (footprint test)")
 a = ap.parse_args()
 cfg = W.CONFIGS[a.config]
 b, (qo, do, qd) = W.gen_batch_device(cfg, n_queries=a.queries)
 nq = b.n_queries
 jobs = []
-for q in range(nq):
+for r in range(a.runs or nq):
+    q = r % nq
     for alpha in cfg.alphas:
         jobs.append(BanditJob(BanditConfig(k=cfg.k, alpha_ef=alpha, seed=(0, q)), int(qd[q + 1] - qd[q]),
                               int(qo[q + 1] - qo[q]), q, int(qd[q]), (-1.0, 1.0), selection=a.selection))
@@ -33,7 +35,7 @@ prof = None
 if a.phases:
     import ctypes
     from paper_2602_02827_b200 import _lib
-    prof = torch.zeros(len(jobs) * 8, dtype=torch.int64, device="cuda")
+    prof = torch.zeros(len(jobs) * 16, dtype=torch.int64, device="cuda")
     _lib.load().cbx_bandit_set_profile(ctypes.c_void_p(prof.data_ptr()))
 elem = b.d_tokens.element_size()
 for it in range(a.iters):
@@ -59,8 +61,9 @@ for it in range(a.iters):
           f"coverage mean {cov.mean():.4f} [{cov.min():.4f}, {cov.max():.4f}], "
           f"{iters / ms * 1e3 / 1e6:.3f} M iter/s aggregate")
     if prof is not None:
-        ph = prof.view(-1, 8).cpu().numpy().astype(np.float64)
+        ph = prof.view(-1, 16).cpu().numpy().astype(np.float64)
         its = np.array([r.iterations for r in res], dtype=np.float64)
-        names = ["scan", "decide", "reveal", "update", "warmup", "total"]
-        per_it = ph[:, :6].sum(0) / its.sum()
+        names = ["scan", "decide", "reveal", "trees", "warmup", "total", "row_update", "sync",
+                 "ru_setup", "ru_welford", "ru_exactsum", "ru_interval", "p12", "p13", "p14", "p15"]
+        per_it = ph[:, :16].sum(0) / its.sum()
         print("  cycles/iteration: " + ", ".join(f"{n}={v:.0f}" for n, v in zip(names, per_it)))
