@@ -14,6 +14,10 @@ The JSON line also carries the Col-Bandit loop (P2) on the same batch
 ("bandit": one CTA per query, default BanditConfig, seed (0, q)), with its
 revealed-cell throughput, gather bandwidth and CPU-oracle parity.
 
+"bandit_sharded" is the document-sharded Col-Bandit on cfg4 (one query, 100k
+candidates split over the ranks, one 8-byte all-reduce per iteration), with
+its single-GPU persistent-kernel time and trace equality beside it.
+
 ``--impl reference`` times the reference's CPU algorithm (the oracle port in
 oracle/maxsim_ref: float64 GEMM + column max + math.fsum + lexsort) on the
 box's host cores, one process per core, for the same metric and config.
@@ -328,8 +332,76 @@ def run_ours(args, rank, world, local_rank):
         s1 = run_stage1(args, rank, world)
         if rank == 0:
             result["stage1"] = s1
+    # ------------------------------------------------ P2 document-sharded over the ranks (cfg4)
+    if not args.no_p2_sharded:
+        torch.cuda.empty_cache()
+        ps = run_p2_sharded(args, rank, world)
+        if rank == 0:
+            result["bandit_sharded"] = ps
     if rank == 0:
         print(json.dumps(result), flush=True)
+
+
+def run_p2_sharded(args, rank, world):
+    """cfg4 (one query, 100k candidates) Col-Bandit with the documents split over the ranks: each rank holds
+    its shard's tokens, keeps the replicated run state and exchanges the revealed value every iteration
+    (sharded.drive: cbx_bandit_shard_step + NCCL all-reduce MAX, 64 iterations per CUDA graph). Rank 0 also
+    runs the single-GPU persistent kernel on the whole pool and checks the traces are identical."""
+    import numpy as np
+    import torch
+
+    from paper_2602_02827_b200 import BanditConfig, BanditJob, run_batch
+    from paper_2602_02827_b200 import workloads as W
+    from paper_2602_02827_b200.batch import TokenBatch
+    from paper_2602_02827_b200.dist import balanced_ranges
+    from paper_2602_02827_b200.sharded import ShardedBanditRun, allreduce_exchange, drive
+
+    cfg = W.CONFIGS["cfg4"]
+    b, (qo, do, qd) = W.gen_batch_device(cfg, n_queries=1, seed=0)  # the same pool on every rank
+    N, T = b.n_docs, int(qo[1] - qo[0])
+    bc = BanditConfig(k=cfg.k, seed=(0, 0))
+    lo, hi = balanced_ranges(do, world)[rank]
+    local = np.zeros(N + 1, np.int64)
+    local[lo:hi + 1] = do[lo:hi + 1] - do[lo]
+    local[hi + 1:] = do[hi] - do[lo]
+    shard_tokens = b.d_tokens[int(do[lo]):int(do[hi])].clone()
+    sb = TokenBatch.from_device(b.q_tokens, b.q_tok_off, shard_tokens, torch.from_numpy(local).cuda(), b.q_doc_off,
+                                False, host_offsets=(qo, local, qd))
+    single = None
+    if rank == 0:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        single = run_batch([BanditJob(bc, N, T, 0, 0, (-1.0, 1.0))], batch=b)[0]
+        e1.record()
+        torch.cuda.synchronize()
+        single_ms = e0.elapsed_time(e1)
+    del b
+    exchange = allreduce_exchange() if world > 1 else (lambda x, n: None)
+    run = ShardedBanditRun(sb, (lo, hi), bc)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = drive(run, exchange)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank != 0:
+        return None
+    return {"what": "Col-Bandit run() on one cfg4 query (100k docs, Lq=32, d=128, f16, K=100), documents sharded "
+                    f"over {world} rank(s) by token count; replicated run state, one 8-byte all-reduce MAX per "
+                    "iteration (sharded.drive, 64 iterations per CUDA graph)",
+            "ranks": world, "ms": ms, "iterations": res.iterations, "reveals": len(res.reveals),
+            "us_per_iteration": ms * 1e3 / res.iterations,
+            "revealed_cells_per_s": len(res.reveals) / (ms / 1e3),
+            "single_gpu_persistent_ms": single_ms,
+            "trace_equal_single_gpu": res.reveals == single.reveals and res.topk == single.topk,
+            "exchange": "none (1 rank)" if world == 1 else "NCCL all-reduce MAX, 8 B per iteration, NVLink",
+            "gpu_launches": run.steps}
 
 
 def run_stage1(args, rank, world):
@@ -582,6 +654,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-bandit", action="store_true")
     ap.add_argument("--no-stage1", action="store_true")
+    ap.add_argument("--no-p2-sharded", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

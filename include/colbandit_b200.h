@@ -256,6 +256,33 @@ CBX_API int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_
                            int32_t* trace_i, int32_t* trace_t, double* trace_v,
                            cbx_bandit_out* out, void* stream);
 
+/* Document-sharded Col-Bandit (BASELINE cfg4 over several GPUs).
+ * One run whose N documents are split over ranks. Every rank keeps the whole
+ * compact run state (row statistics, intervals, selection trees, PCG64 stream)
+ * and takes the identical decisions; it holds, and reveals, only the tokens of
+ * its own rows [own_lo, own_hi) (``b`` indexes rows globally: documents of
+ * other ranks may be empty). A call advances the run to its next exchange
+ * point: it applies the cell values of the previous exchange, decides, and
+ * writes the cells it owns into ``xchg`` as signed-order keys (INT64_MIN for
+ * cells it does not own). Between calls the caller combines ``xchg`` across
+ * ranks with an all-reduce MAX, over the slot count named by the int32 at
+ * offset 0 of ``step_state`` (CBX_SHARD_REVEAL: 1 slot; CBX_SHARD_WARMUP: the
+ * warm-up cells, N for epsilon-greedy or n_warm; CBX_SHARD_DONE: finished,
+ * further calls return at once). ``step_state``: CBX_BANDIT_STEP_BYTES of
+ * device memory, zeroed before the first call (first = 1). ``xchg``: int64
+ * [max(N, n_warm, 1)]. Outputs as cbx_bandit_run once DONE, identical on every
+ * rank; the trace is reveal-for-reveal the single-GPU trace. */
+#define CBX_BANDIT_STEP_BYTES 256
+#define CBX_SHARD_REVEAL 0
+#define CBX_SHARD_WARMUP 1
+#define CBX_SHARD_DONE 2
+CBX_API int cbx_bandit_shard_step(const cbx_batch* b, const double* matrix, int64_t ld_matrix,
+                                  const cbx_bandit_run_desc* run, int64_t own_lo, int64_t own_hi, int first,
+                                  const double* bounds_lo, const double* bounds_hi, const int32_t* warm_cells,
+                                  void* state, size_t state_bytes, void* step_state, int64_t* xchg,
+                                  int32_t* topk, int32_t max_k, int32_t* trace_i, int32_t* trace_t,
+                                  double* trace_v, cbx_bandit_out* out, void* stream);
+
 /* Profiling hook: when set (device pointer to n_runs * 16 uint64), every
  * following cbx_bandit_run writes per-run SM-cycle counters of its phases
  * [scan, decide, reveal, trees, warm-up, total, row update, sync, and the

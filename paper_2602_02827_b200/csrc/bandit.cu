@@ -105,7 +105,30 @@ struct BanditParams {
   double* trace_v;
   cbx_bandit_out* out;
   unsigned long long* prof;  // optional per-run phase cycle counters (cbx_bandit_set_profile)
+  // document-sharded run (cbx_bandit_shard_step): one run, state resumed across launches
+  int shard, first;
+  int64_t own_lo, own_hi;   // rows whose tokens this rank holds
+  int64_t* xchg;            // exchange slots, all-reduced with MAX between launches
+  struct BdStep* step;
 };
+
+// Resumable loop state of a sharded run (lives in global memory between launches).
+struct BdStep {
+  int32_t phase;     // CBX_SHARD_*: what the caller must exchange next
+  int32_t pending;   // 0 none, 1 reveal value in xchg[0], 2 warm-up values in xchg[0..warm_m)
+  int32_t status, iterations;
+  int64_t n_reveals;
+  int32_t i_star, t_star, swap_in, swap_out;
+  int64_t warm_base, warm_m;
+  uint64_t sh, sl, ih, il;
+  uint32_t has32, buf;
+  int32_t warmed, pad;
+};
+static_assert(sizeof(BdStep) <= CBX_BANDIT_STEP_BYTES, "step state");
+
+// cell value <-> exchange slot: signed order == value order, INT64_MIN = "not mine"
+__device__ __forceinline__ int64_t xchg_key(uint64_t ordkey) { return (int64_t)(ordkey ^ 0x8000000000000000ull); }
+__device__ __forceinline__ uint64_t xchg_ord(int64_t k) { return (uint64_t)k ^ 0x8000000000000000ull; }
 
 // ----------------------------------------------------------------- Python semantics
 __device__ __forceinline__ double pymin(double a, double b) { return b < a ? b : a; }
@@ -808,10 +831,19 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
   };
 
   // ------------------------------------------------------------ initial state (all n = 0)
+  BdStep* const step = P.step;
+  const bool resume = P.shard && !P.first;
+  if (P.shard && step->phase == CBX_SHARD_DONE) return;
   if (tid == 0) {
-    ctrl->status = 0;
-    ctrl->n_reveals = 0;
-    ctrl->iterations = 0;
+    ctrl->status = resume ? step->status : 0;
+    ctrl->n_reveals = resume ? step->n_reveals : 0;
+    ctrl->iterations = resume ? step->iterations : 0;
+    if (resume) {
+      ctrl->i_star = step->i_star;
+      ctrl->t_star = step->t_star;
+      ctrl->swap_in = step->swap_in;
+      ctrl->swap_out = step->swap_out;
+    }
   }
   for (int n = tid; n <= BD_MAX_T; n += BD_THREADS) {
     double a = 0.0, b = 0.0;
@@ -827,7 +859,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
   }
   __syncthreads();
   const uint64_t full_mask = TC >= 64 ? ~0ull : ((1ull << TC) - 1ull);
-  for (int i = tid; i < N; i += BD_THREADS) {
+  for (int i = resume ? N : tid; i < N; i += BD_THREADS) {
     rv.mean[i] = 0.0;
     rv.m2[i] = 0.0;
     rv.fx[i] = 0;
@@ -850,16 +882,54 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
     rv.ucb[i] = u;
   }
   __syncthreads();
-  rebuild();
+  if (!resume) rebuild();
 
   Pcg64 rng;
-  rng.sh = R.rng.state_hi;
-  rng.sl = R.rng.state_lo;
-  rng.ih = R.rng.inc_hi;
-  rng.il = R.rng.inc_lo;
-  rng.has32 = R.rng.has_uint32;
-  rng.buf = R.rng.uinteger;
-  bool warmed = (K == N) || (R.explore_mode == CBX_UNIFORM_ROW);
+  rng.sh = resume ? step->sh : R.rng.state_hi;
+  rng.sl = resume ? step->sl : R.rng.state_lo;
+  rng.ih = resume ? step->ih : R.rng.inc_hi;
+  rng.il = resume ? step->il : R.rng.inc_lo;
+  rng.has32 = resume ? step->has32 : R.rng.has_uint32;
+  rng.buf = resume ? step->buf : R.rng.uinteger;
+  bool warmed = resume ? step->warmed != 0 : ((K == N) || (R.explore_mode == CBX_UNIFORM_ROW));
+  int resume_kind = resume ? step->pending : 0;
+  // sharded run: park the loop at an exchange point (thread 0 holds the live generator)
+  auto park = [&](int pending, int phase, int64_t wbase, int64_t wm) {
+    if (tid == 0) {
+      step->phase = phase;
+      step->pending = pending;
+      step->status = ctrl->status;
+      step->iterations = ctrl->iterations;
+      step->n_reveals = ctrl->n_reveals;
+      step->i_star = ctrl->i_star;
+      step->t_star = ctrl->t_star;
+      step->swap_in = ctrl->swap_in;
+      step->swap_out = ctrl->swap_out;
+      step->warm_base = wbase;
+      step->warm_m = wm;
+      step->sh = rng.sh;
+      step->sl = rng.sl;
+      step->ih = rng.ih;
+      step->il = rng.il;
+      step->has32 = rng.has32;
+      step->buf = rng.buf;
+      step->warmed = warmed ? 1 : 0;
+    }
+  };
+  // apply the m warm-up reveals recorded at trace[base, base + m) (bandit.py:285-296)
+  auto warmup_apply = [&](int64_t base, int64_t m) {
+    if (R.explore_mode == CBX_EPSILON_GREEDY) {
+      for (int i = tid; i < N; i += BD_THREADS)
+        if (!reveal_update(i, tr_t[base + i], tr_v[base + i])) ctrl->status = 2;
+    } else if (tid == 0) {
+      for (int64_t s2 = 0; s2 < m; ++s2)
+        if (!reveal_update(tr_i[base + s2], tr_t[base + s2], tr_v[base + s2])) ctrl->status = 2;
+    }
+    __syncthreads();
+    if (m > 0) rebuild();
+    if (tid == 0) ctrl->n_reveals = base + m;
+    __syncthreads();
+  };
   const double eps = R.explore_mode == CBX_UNIFORM_ROW ? 1.0 : R.epsilon;
   const int64_t total_cells = (int64_t)N * TC;
   int term = CBX_TERM_SEPARATION;
@@ -868,6 +938,8 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
 
   while (true) {
     BD_PHASE(3);
+    int i_star, t_star;
+    if (resume_kind == 0) {
     // ---------------------------------------------------------- boundary selection
     if (!use_tree) {
       Cand c[4] = {{0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}};
@@ -974,54 +1046,46 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       // -------------------------------------------------------- lazy warm-up (bandit.py:285-296)
       warmed = true;
       const int64_t base = ctrl->n_reveals;
-      int64_t m;
+      const int64_t m = R.explore_mode == CBX_EPSILON_GREEDY ? N : R.n_warm;
       if (R.explore_mode == CBX_EPSILON_GREEDY) {
-        m = N;
         if (tid == 0)
           for (int i = 0; i < N; ++i) {
             tr_i[base + i] = i;
             tr_t[base + i] = (int32_t)rng.integers((uint32_t)TC);
           }
-        __syncthreads();
-        // one warp per document: every token once, dotted with the row's warm-up query token
-        for (int i = warp; i < N; i += BD_WARPS) {
-          const double v = cell_warp(i, tr_t[base + i]);
-          if (lane == 0) rv.wkey[i] = ord_key(v);
-        }
-        __syncthreads();
-        for (int i = tid; i < N; i += BD_THREADS) {
-          const double v = ord_val(rv.wkey[i]);
-          tr_v[base + i] = v;
-          if (!reveal_update(i, tr_t[base + i], v)) ctrl->status = 2;
-        }
       } else {
-        m = R.n_warm;
         const int32_t* wc = P.warm_cells + R.warm_off;
         for (int64_t s = tid; s < m; s += BD_THREADS) {
           tr_i[base + s] = wc[s] / TC;
           tr_t[base + s] = wc[s] % TC;
         }
-        __syncthreads();
-        for (int64_t s = warp; s < m; s += BD_WARPS) {
-          const double v = cell_warp(tr_i[base + s], tr_t[base + s]);
-          if (lane == 0) tr_v[base + s] = v;
-        }
-        __syncthreads();
-        if (tid == 0)
-          for (int64_t s2 = 0; s2 < m; ++s2)
-            if (!reveal_update(tr_i[base + s2], tr_t[base + s2], tr_v[base + s2])) ctrl->status = 2;
       }
       __syncthreads();
-      if (m > 0) rebuild();
-      if (tid == 0) ctrl->n_reveals = base + m;
+      // one warp per cell: every token of the row once, dotted with its query token (a shard: its rows only)
+      for (int64_t s = warp; s < m; s += BD_WARPS) {
+        const int i = tr_i[base + s];
+        const bool own = !P.shard || (i >= P.own_lo && i < P.own_hi);
+        const double v = own ? cell_warp(i, tr_t[base + s]) : 0.0;
+        if (lane == 0) {
+          if (P.shard) P.xchg[s] = own ? xchg_key(ord_key(v)) : INT64_MIN;
+          else tr_v[base + s] = v;
+        }
+      }
+      if (P.shard) {
+        park(2, CBX_SHARD_WARMUP, base, m);
+        return;
+      }
       __syncthreads();
+      warmup_apply(base, m);
       BD_PHASE(4);
       continue;
     }
 
     // ---------------------------------------------------------- reveal one cell
-    const int i_star = ctrl->i_star, t_star = ctrl->t_star;
-    if (tokens) {
+    i_star = ctrl->i_star;
+    t_star = ctrl->t_star;
+    const bool own = !P.shard || (i_star >= P.own_lo && i_star < P.own_hi);
+    if (tokens && own) {
       double best = tokens_max<T, G, VPL, B>(dtok, dto[i_star], dto[i_star + 1], qtok + (int64_t)t_star * dim, dim,
                                              gid, NGROUPS, sub, init_cell, warp, BD_WARPS, &ctrl->cellkey);
 #pragma unroll
@@ -1032,10 +1096,35 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       if (lane == 0) atomicMax(&ctrl->cellkey, (unsigned long long)ord_key(best));
       __syncthreads();
     }
+    if (P.shard) {
+      if (tid == 0) {
+        const double v = tokens ? ord_val(ctrl->cellkey) : P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
+        P.xchg[0] = own ? xchg_key(ord_key(v)) : INT64_MIN;
+      }
+      park(1, CBX_SHARD_REVEAL, 0, 0);
+      return;
+    }
+    } else if (resume_kind == 2) {
+      // -------------------------------------------------------- sharded: warm-up values from the exchange
+      resume_kind = 0;
+      const int64_t base = step->warm_base, m = step->warm_m;
+      for (int64_t s = tid; s < m; s += BD_THREADS) tr_v[base + s] = ord_val(xchg_ord(P.xchg[s]));
+      __syncthreads();
+      warmup_apply(base, m);
+      continue;
+    } else {
+      // -------------------------------------------------------- sharded: the revealed value from the exchange
+      resume_kind = 0;
+      i_star = ctrl->i_star;
+      t_star = ctrl->t_star;
+      if (tid == 0) ctrl->cellkey = xchg_ord(P.xchg[0]);
+      __syncthreads();
+    }
     BD_PHASE(2);
     int partner = -1;
     if (tid == 0) {
-      const double v = tokens ? ord_val(ctrl->cellkey) : P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
+      const double v = (tokens || P.shard) ? ord_val(ctrl->cellkey)
+                                           : P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
       const int64_t pos = ctrl->n_reveals;
       tr_i[pos] = i_star;
       tr_t[pos] = t_star;
@@ -1121,6 +1210,10 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
     o.status = ctrl->status;
     o.pad = 0;
     P.out[blockIdx.x] = o;
+    if (P.shard) {
+      step->phase = CBX_SHARD_DONE;
+      step->pending = 0;
+    }
     if (P.prof) {
       ph[5] = clock64() - tcs;
       for (int k = 0; k < 16; ++k) P.prof[blockIdx.x * 16 + k] = ph[k];
@@ -1170,6 +1263,18 @@ static int dispatch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, c
   return fail(CBX_EINVAL, "bandit: embedding rows above 2 KiB are not supported");
 }
 
+struct ShardArgs {
+  int64_t own_lo, own_hi;
+  int first;
+  int64_t* xchg;
+  void* step;
+};
+static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_matrix, const cbx_bandit_run_desc* runs,
+                         int64_t n_runs, int32_t max_rows, const double* bounds_lo, const double* bounds_hi,
+                         const int32_t* warm_cells, void* state, size_t state_bytes, int32_t* topk, int32_t max_k,
+                         int32_t* trace_i, int32_t* trace_t, double* trace_v, cbx_bandit_out* out, void* stream,
+                         const ShardArgs* sa);
+
 extern "C" {
 
 void cbx_bandit_set_profile(void* counters) { g_bandit_prof = static_cast<unsigned long long*>(counters); }
@@ -1189,6 +1294,31 @@ int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix, 
   if (!b && !matrix) return fail(CBX_EINVAL, "bandit: need token embeddings or a cell matrix");
   if (n_runs > 0x7FFFFFFF) return fail(CBX_EINVAL, "bandit: too many runs");
   if (max_rows <= 0) return fail(CBX_EINVAL, "bandit: max_rows must be positive");
+  return launch_params(b, matrix, ld_matrix, runs, n_runs, max_rows, bounds_lo, bounds_hi, warm_cells, state,
+                       state_bytes, topk, max_k, trace_i, trace_t, trace_v, out, stream, nullptr);
+}
+
+int cbx_bandit_shard_step(const cbx_batch* b, const double* matrix, int64_t ld_matrix, const cbx_bandit_run_desc* run,
+                          int64_t own_lo, int64_t own_hi, int first, const double* bounds_lo, const double* bounds_hi,
+                          const int32_t* warm_cells, void* state, size_t state_bytes, void* step_state,
+                          int64_t* xchg, int32_t* topk, int32_t max_k, int32_t* trace_i, int32_t* trace_t,
+                          double* trace_v, cbx_bandit_out* out, void* stream) {
+  if (!run || !out || !topk || !trace_i || !trace_t || !trace_v || !state || !step_state || !xchg)
+    return fail(CBX_EINVAL, "bandit shard: NULL buffer");
+  if (!b && !matrix) return fail(CBX_EINVAL, "bandit shard: need token embeddings or a cell matrix");
+  if (own_lo < 0 || own_hi < own_lo) return fail(CBX_EINVAL, "bandit shard: bad owned row range");
+  ShardArgs sa{own_lo, own_hi, first, xchg, step_state};
+  return launch_params(b, matrix, ld_matrix, run, 1, 0x7FFFFFFF, bounds_lo, bounds_hi, warm_cells, state, state_bytes,
+                       topk, max_k, trace_i, trace_t, trace_v, out, stream, &sa);
+}
+
+}  // extern "C"
+
+static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_matrix, const cbx_bandit_run_desc* runs,
+                         int64_t n_runs, int32_t max_rows, const double* bounds_lo, const double* bounds_hi,
+                         const int32_t* warm_cells, void* state, size_t state_bytes, int32_t* topk, int32_t max_k,
+                         int32_t* trace_i, int32_t* trace_t, double* trace_v, cbx_bandit_out* out, void* stream,
+                         const ShardArgs* sa) {
   if (b) {
     const size_t es = dtype_size(b->dtype);
     if ((b->dim * es) % 16 != 0) return fail(CBX_EINVAL, "bandit: token rows must be a multiple of 16 bytes");
@@ -1229,9 +1359,15 @@ int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix, 
   P.trace_v = trace_v;
   P.out = out;
   P.prof = g_bandit_prof;
+  P.shard = sa ? 1 : 0;
+  P.first = sa ? sa->first : 0;
+  P.own_lo = sa ? sa->own_lo : 0;
+  P.own_hi = sa ? sa->own_hi : 0;
+  P.xchg = sa ? sa->xchg : nullptr;
+  P.step = sa ? static_cast<BdStep*>(sa->step) : nullptr;
   size_t smem = 128 + sizeof(Cand) * 4 * BD_WARPS + 2 * sizeof(double) * (BD_MAX_T + 1);
   smem = align_up(smem, 16);
-  P.use_smem = max_rows <= BD_SMEM_ROWS ? 1 : 0;
+  P.use_smem = (max_rows <= BD_SMEM_ROWS && !sa) ? 1 : 0;  // a sharded run resumes from global state
   if (P.use_smem) smem += (size_t)(max_rows + BD_ROW_SLACK) * ROW_STRIDE + 64;
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1246,5 +1382,3 @@ int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix, 
   }
   return fail(CBX_EINVAL, "bandit: unknown dtype");
 }
-
-}  // extern "C"
