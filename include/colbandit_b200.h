@@ -205,6 +205,8 @@ typedef struct cbx_pcg64 {
  * cells with numpy's Generator.choice (bandit.py:152) and passes them, in
  * draw order, at warm_cells[warm_off ...] together with the generator state
  * after that draw; every other draw happens on the device. */
+#define CBX_BANDIT_TREE 1
+#define CBX_BANDIT_PREWARMED 2
 typedef struct cbx_bandit_run_desc {
   int64_t query;          /* token source: query index in the batch           */
   int64_t row_begin;      /* global doc index (token source) or matrix row of row 0 */
@@ -213,8 +215,10 @@ typedef struct cbx_bandit_run_desc {
   int32_t k;              /* Top-K target, 1..N (k == 0 is answered on the host) */
   int32_t explore_mode;   /* CBX_EPSILON_GREEDY / CBX_STATIC_WARMUP / CBX_UNIFORM_ROW */
   int32_t n_warm;         /* static warm-up cell count                        */
-  int32_t flags;          /* bit 0: boundary selection through tournament trees (O(log N) per
-                             reveal) instead of a full pool scan; the host sets it for large pools */
+  int32_t flags;          /* bit 0 (CBX_BANDIT_TREE): boundary selection through tournament trees
+                             (O(log N) per reveal) instead of a full pool scan;
+                             bit 1 (CBX_BANDIT_PREWARMED): cbx_bandit_prewarm computed the warm-up
+                             cells into trace[trace_off, +m) before the loop kernel runs */
   int64_t warm_off;       /* offset of this run's cells in warm_cells         */
   double alpha_ef;
   double epsilon;
@@ -255,6 +259,18 @@ CBX_API int cbx_bandit_run(const cbx_batch* b, const double* matrix, int64_t ld_
                            int32_t* topk, int32_t max_k,
                            int32_t* trace_i, int32_t* trace_t, double* trace_v,
                            cbx_bandit_out* out, void* stream);
+
+/* Warm-up pre-pass for token-backed runs whose flags carry CBX_BANDIT_PREWARMED:
+ * draws each run's warm-up cells (epsilon-greedy: one column per row from the
+ * run's PCG64 stream; static-warmup: warm_cells) and computes their float64
+ * values with a grid of warps (HBM-bound), into trace_{i,t,v}[trace_off + s],
+ * s < m. warm_prefix: device int64[n_runs + 1], exclusive prefix sum of each
+ * run's pre-warmed cell count (0 for other runs); total_cells = its last entry.
+ * Launch it on the same stream before cbx_bandit_run with the same arguments;
+ * the loop then replays the draws and uses the values (identical results). */
+CBX_API int cbx_bandit_prewarm(const cbx_batch* b, const cbx_bandit_run_desc* runs, int64_t n_runs,
+                               const int64_t* warm_prefix, int64_t total_cells, const int32_t* warm_cells,
+                               int32_t* trace_i, int32_t* trace_t, double* trace_v, void* stream);
 
 /* Document-sharded Col-Bandit (BASELINE cfg4 over several GPUs).
  * One run whose N documents are split over ranks. Every rank keeps the whole

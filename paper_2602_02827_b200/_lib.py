@@ -21,6 +21,7 @@ CBX_EPSILON_GREEDY, CBX_STATIC_WARMUP, CBX_UNIFORM_ROW = 0, 1, 2
 CBX_TERM_SEPARATION, CBX_TERM_EXHAUSTION = 0, 1
 CBX_BANDIT_ROW_SLACK = 64
 CBX_BANDIT_TREE = 1
+CBX_BANDIT_PREWARMED = 2
 CBX_BANDIT_STEP_BYTES = 256
 CBX_SHARD_REVEAL, CBX_SHARD_WARMUP, CBX_SHARD_DONE = 0, 1, 2
 
@@ -115,6 +116,7 @@ SIGNATURES = {
     "cbx_bandit_state_bytes": (_SZ, [_I64]),
     "cbx_bandit_set_profile": (None, [_P]),
     "cbx_bandit_run": (_I, [_P, _P, _I64, _P, _I64, _I32, _P, _P, _P, _P, _SZ, _P, _I32, _P, _P, _P, _P, _P]),
+    "cbx_bandit_prewarm": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P]),
     "cbx_bandit_shard_step": (_I, [_P, _P, _I64, _P, _I64, _I64, _I, _P, _P, _P, _P, _SZ, _P, _P, _P, _I32, _P, _P,
                                    _P, _P, _P]),
 }

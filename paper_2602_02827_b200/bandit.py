@@ -26,7 +26,8 @@ import numpy as np
 from . import _lib
 from .bounds import CellBounds, RadiusConfig
 
-__all__ = ["BanditConfig", "RunResult", "EXPLORE_MODES", "run", "run_batch", "ceil_cells", "select_ambiguous",
+__all__ = ["BanditConfig", "RunResult", "EXPLORE_MODES", "run", "run_batch", "prepare_batch", "launch_batch",
+           "ceil_cells", "select_ambiguous",
            "select_token", "static_warmup", "init_one_per_row", "BanditJob"]
 
 EXPLORE_MODES = ("epsilon-greedy", "static-warmup", "uniform-row")
@@ -159,8 +160,39 @@ def _rng_state(seed, explore_mode, gamma_init, total_cells):
     return p, warm
 
 
-def run_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, return_traces: bool = True, sync: bool = True):
-    """Launch every job in one kernel; returns a list of RunResult (or raw device outputs if sync=False)."""
+def _sm_count() -> int:
+    import torch
+
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+def _warms_up(job: BanditJob, uniform) -> bool:
+    """Will the run reach its lazy warm-up (i.e. fail the stop test at iteration 1, bandit.py:281-296)?
+
+    Only decides whether the warm-up cells are computed ahead by cbx_bandit_prewarm (a performance
+    choice): a run that is not pre-warmed computes them inside the loop kernel, so a borderline case is
+    answered False. Initial intervals: LCB = sum(lo), UCB = sum(hi), proxy = midpoint (bounds.py:211-263).
+    """
+    cfg, N = job.cfg, job.n_rows
+    if cfg.explore_mode == "uniform-row" or cfg.k >= N:
+        return False
+    if uniform:
+        return uniform[0] < uniform[1]
+    b = job.bounds
+    h_lo, h_hi = b.lo.sum(axis=1), b.hi.sum(axis=1)
+    proxy = 0.5 * (h_lo + h_hi)
+    order = np.lexsort((np.arange(N), -proxy))
+    top, rest = order[: cfg.k], order[cfg.k:]
+    lcb_plus, ucb_minus = h_lo[top].min(), h_hi[rest].max()
+    return bool(lcb_plus < ucb_minus - 1e-9 * (abs(lcb_plus) + abs(ucb_minus) + 1.0))
+
+
+def prepare_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, prewarm: bool | None = None) -> dict:
+    """Host side of a batched launch: validate the jobs, seed the generators, build the run descriptors and
+    move them (and any per-cell bounds) to the device; outputs are allocated. ``launch_batch`` then issues
+    the kernels. ``prewarm`` (None = auto: when the runs fit one CTA per SM) computes the warm-up cells of
+    token-backed runs with one HBM-bound cbx_bandit_prewarm launch ahead of the loop kernel (same values,
+    same traces)."""
     torch = _lib.require_cuda()
     lib = _lib.load()
     if batch is None and matrix is None:
@@ -172,6 +204,11 @@ def run_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, return_traces:
     max_rows = max_k = 1
     results: list = [None] * n
     live = []
+    warm_counts = []
+    # the in-loop warm-up gathers with one CTA; with at most one run per SM that CTA is latency bound and
+    # a grid-wide pre-pass wins (measured: cfg3 128 runs, cfg4 1 run); with more runs the loop kernels
+    # already keep HBM busy during their warm-ups (cfg2 256 runs: no gain)
+    prewarm_on = prewarm if prewarm is not None else len(jobs) <= _sm_count()
     for r, job in enumerate(jobs):
         cfg = job.cfg
         N, T = int(job.n_rows), int(job.n_cols)
@@ -206,13 +243,17 @@ def run_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, return_traces:
             raise ValueError(f"selection must be 'auto', 'scan' or 'tree', got {job.selection!r}")
         tree = job.selection == "tree" or (job.selection == "auto" and N > TREE_ROWS)
         d.flags = _lib.CBX_BANDIT_TREE if tree else 0
+        pre = prewarm_on and batch is not None and _warms_up(job, uni)
+        if pre:
+            d.flags |= _lib.CBX_BANDIT_PREWARMED
+        warm_counts.append((N if cfg.explore_mode == "epsilon-greedy" else len(warm)) if pre else 0)
         d.trace_off, d.state_off = tr_off, st_off
         tr_off += N * T
         st_off += N + _lib.CBX_BANDIT_ROW_SLACK
         max_rows, max_k = max(max_rows, N), max(max_k, cfg.k)
     nl = len(live)
     if nl == 0:
-        return results
+        return dict(results=results, live=live)
     dev = torch.device("cuda", torch.cuda.current_device())
     desc_t = torch.frombuffer(bytearray(bytes(descs)[: nl * ctypes.sizeof(_lib.CbxBanditRunDesc)]),
                               dtype=torch.uint8).to(dev)
@@ -227,21 +268,49 @@ def run_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, return_traces:
     tr_v = torch.empty(max(tr_off, 1), dtype=torch.float64, device=dev)
     out_t = torch.empty(nl * ctypes.sizeof(_lib.CbxBanditOut), dtype=torch.uint8, device=dev)
     bstruct = batch.struct() if batch is not None else None
-    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     ld = matrix.shape[1] if matrix is not None else 0
+    wprefix = None
+    if sum(warm_counts):
+        wp = np.zeros(nl + 1, np.int64)
+        np.cumsum(warm_counts, out=wp[1:])
+        wprefix = torch.from_numpy(wp).to(dev)
+    return dict(results=results, live=live, descs=descs, nl=nl, max_rows=max_rows, max_k=max_k, bstruct=bstruct,
+                batch=batch, matrix=matrix, ld=ld, desc_t=desc_t, lo_t=lo_t, hi_t=hi_t, warm_t=warm_t, state=state,
+                state_bytes=state_bytes, topk=topk_t, tr_i=tr_i, tr_t=tr_t, tr_v=tr_v, out=out_t, wprefix=wprefix,
+                n_prewarm=int(sum(warm_counts)))
+
+
+def launch_batch(p: dict):
+    """Issue a prepared batch on the current stream (no host synchronisation); returns the raw outputs."""
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    bref = ctypes.byref(p["bstruct"]) if p["bstruct"] is not None else None
+    if p["wprefix"] is not None:
+        _lib.check(lib.cbx_bandit_prewarm(
+            bref, p["desc_t"].data_ptr(), p["nl"], p["wprefix"].data_ptr(), p["n_prewarm"], ptr(p["warm_t"]),
+            p["tr_i"].data_ptr(), p["tr_t"].data_ptr(), p["tr_v"].data_ptr(), stream), "bandit_prewarm")
+    m = p["matrix"]
     _lib.check(lib.cbx_bandit_run(
-        ctypes.byref(bstruct) if bstruct is not None else None,
-        matrix.data_ptr() if matrix is not None else None, ld,
-        desc_t.data_ptr(), nl, max_rows,
-        lo_t.data_ptr() if lo_t is not None else None, hi_t.data_ptr() if hi_t is not None else None,
-        warm_t.data_ptr() if warm_t is not None else None, state.data_ptr(), state_bytes,
-        topk_t.data_ptr(), max_k, tr_i.data_ptr(), tr_t.data_ptr(), tr_v.data_ptr(), out_t.data_ptr(), stream),
-        "bandit_run")
-    raw = dict(descs=descs, live=live, topk=topk_t, tr_i=tr_i, tr_t=tr_t, tr_v=tr_v, out=out_t,
-               keep=(desc_t, lo_t, hi_t, warm_t, state))
+        bref, m.data_ptr() if m is not None else None, p["ld"], p["desc_t"].data_ptr(), p["nl"], p["max_rows"],
+        ptr(p["lo_t"]), ptr(p["hi_t"]), ptr(p["warm_t"]), p["state"].data_ptr(), p["state_bytes"],
+        p["topk"].data_ptr(), p["max_k"], p["tr_i"].data_ptr(), p["tr_t"].data_ptr(), p["tr_v"].data_ptr(),
+        p["out"].data_ptr(), stream), "bandit_run")
+    return dict(descs=p["descs"], live=p["live"], topk=p["topk"], tr_i=p["tr_i"], tr_t=p["tr_t"], tr_v=p["tr_v"],
+                out=p["out"], keep=p)
+
+
+def run_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, return_traces: bool = True, sync: bool = True,
+              prewarm: bool | None = None):
+    """Launch every job in one kernel; returns a list of RunResult (or raw device outputs if sync=False)."""
+    p = prepare_batch(jobs, batch, matrix, prewarm)
+    if not p["live"]:
+        return p["results"]
+    raw = launch_batch(p)
     if not sync:
         return raw
-    return collect(raw, jobs, results, return_traces)
+    return collect(raw, jobs, p["results"], return_traces)
 
 
 def collect(raw, jobs, results=None, return_traces: bool = True):

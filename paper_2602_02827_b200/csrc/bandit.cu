@@ -650,7 +650,8 @@ __device__ __forceinline__ double tokens_max(const T* __restrict__ dtok, int64_t
                                              const unsigned long long* shared_best) {
   if constexpr (sizeof(T) == 2 && CBX_BD_SCREEN) {
     constexpr int SG = (G * VPL) / 4 < 1 ? 1 : (G * VPL) / 4;
-    return tokens_max_screen<T, SG, CBX_BD_SCREEN_B>(dtok, j0, j1, q, dim, wid, nwarps, threadIdx.x & 31, init, shared_best);
+    return tokens_max_screen<T, SG, CBX_BD_SCREEN_B>(dtok, j0, j1, q, dim, wid, nwarps, threadIdx.x & 31, init,
+                                                      shared_best);
   } else {
     return tokens_max_dot<T, G, VPL, B>(dtok, j0, j1, q, dim, gid, ngroups, sub, init);
   }
@@ -695,7 +696,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
   if (!P.use_smem) row_base = P.g_rows + (size_t)R.state_off * ROW_STRIDE;
   RowsView rv;
   rv.carve(row_base, N);
-  const bool use_tree = (R.flags & 1) != 0;
+  const bool use_tree = (R.flags & CBX_BANDIT_TREE) != 0;
   Trees tr;
   tr.carve(row_base + align_up_dev(ROW_BYTES * (size_t)N, 16), N);
   ExpStore* g_obs = P.g_obs + R.state_off;
@@ -1047,13 +1048,18 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       warmed = true;
       const int64_t base = ctrl->n_reveals;
       const int64_t m = R.explore_mode == CBX_EPSILON_GREEDY ? N : R.n_warm;
+      // cells computed by cbx_bandit_prewarm already sit in trace[0, m) (the warm-up is the first reveal)
+      const bool pre = (R.flags & CBX_BANDIT_PREWARMED) && base == 0 && !P.shard;
       if (R.explore_mode == CBX_EPSILON_GREEDY) {
         if (tid == 0)
           for (int i = 0; i < N; ++i) {
-            tr_i[base + i] = i;
-            tr_t[base + i] = (int32_t)rng.integers((uint32_t)TC);
+            const int32_t t = (int32_t)rng.integers((uint32_t)TC);
+            if (!pre) {
+              tr_i[base + i] = i;
+              tr_t[base + i] = t;
+            }
           }
-      } else {
+      } else if (!pre) {
         const int32_t* wc = P.warm_cells + R.warm_off;
         for (int64_t s = tid; s < m; s += BD_THREADS) {
           tr_i[base + s] = wc[s] / TC;
@@ -1062,7 +1068,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       }
       __syncthreads();
       // one warp per cell: every token of the row once, dotted with its query token (a shard: its rows only)
-      for (int64_t s = warp; s < m; s += BD_WARPS) {
+      for (int64_t s = warp; s < (pre ? 0 : m); s += BD_WARPS) {
         const int i = tr_i[base + s];
         const bool own = !P.shard || (i >= P.own_lo && i < P.own_hi);
         const double v = own ? cell_warp(i, tr_t[base + s]) : 0.0;
@@ -1222,6 +1228,77 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
 #undef BD_PHASE
 }
 
+// ----------------------------------------------------------------- warm-up pre-pass
+// The lazy warm-up (bandit.py:285-296) is the first reveal of a run: one cell
+// per row (epsilon-greedy; columns from the run's own PCG64 stream) or the
+// host-drawn static sample. Inside the loop kernel a CTA gathers its N
+// documents with 8 warps, one document at a time each — latency bound. Here
+// the cells of every pre-warmed run are computed by a grid of warps with many
+// documents in flight per SM (HBM bound), straight into the run's trace slots
+// [trace_off, trace_off + m); the loop kernel then only replays the draws to
+// advance its generator. Same cell function, so the values are the ones the
+// loop kernel would compute.
+__global__ void warm_draw_kernel(const cbx_bandit_run_desc* __restrict__ runs, int n_runs,
+                                 const int32_t* __restrict__ warm_cells, int32_t* tr_i, int32_t* tr_t) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_runs) return;
+  const cbx_bandit_run_desc& R = runs[r];
+  if (!(R.flags & CBX_BANDIT_PREWARMED)) return;
+  int32_t* ti = tr_i + R.trace_off;
+  int32_t* tt = tr_t + R.trace_off;
+  if (R.explore_mode == CBX_EPSILON_GREEDY) {
+    Pcg64 rng;
+    rng.sh = R.rng.state_hi;
+    rng.sl = R.rng.state_lo;
+    rng.ih = R.rng.inc_hi;
+    rng.il = R.rng.inc_lo;
+    rng.has32 = R.rng.has_uint32;
+    rng.buf = R.rng.uinteger;
+    for (int i = 0; i < R.n_rows; ++i) {
+      ti[i] = i;
+      tt[i] = (int32_t)rng.integers((uint32_t)R.n_cols);
+    }
+  } else {
+    const int32_t* wc = warm_cells + R.warm_off;
+    for (int s = 0; s < R.n_warm; ++s) {
+      ti[s] = wc[s] / R.n_cols;
+      tt[s] = wc[s] % R.n_cols;
+    }
+  }
+}
+
+template <typename T, int G, int VPL>
+__global__ void __launch_bounds__(256) warm_cells_kernel(const BanditParams P, int n_runs, const int64_t* wprefix) {
+  constexpr int GW = G <= 32 ? G : 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t total = wprefix[n_runs];
+  const T* dtok = static_cast<const T*>(P.d_tokens);
+  const double init_cell = P.clamp_negative ? 0.0 : -INFINITY;
+  for (int64_t g = w0; g < total; g += nw) {
+    int lo = 0, hi = n_runs;  // run r with wprefix[r] <= g < wprefix[r + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (wprefix[mid] <= g) lo = mid;
+      else hi = mid;
+    }
+    const cbx_bandit_run_desc& R = P.runs[lo];
+    const int64_t slot = R.trace_off + (g - wprefix[lo]);
+    const int i = P.trace_i[slot], t = P.trace_t[slot];
+    const int64_t* dto = P.d_tok_off + R.row_begin;
+    const T* q = static_cast<const T*>(P.q_tokens) + (P.q_tok_off[R.query] + t) * (int64_t)P.dim;
+    double best = tokens_max<T, GW, VPL, (VPL == 1 ? 8 : 4)>(dtok, dto[i], dto[i + 1], q, P.dim, lane / GW, 32 / GW,
+                                                             lane % GW, init_cell, 0, 1, nullptr);
+#pragma unroll
+    for (int o = 16; o >= GW; o >>= 1) {
+      const double w = __shfl_xor_sync(0xffffffffu, best, o);
+      best = w > best ? w : best;
+    }
+    if (lane == 0) P.trace_v[slot] = best;
+  }
+}
+
 }  // namespace cbx
 
 using namespace cbx;
@@ -1310,6 +1387,57 @@ int cbx_bandit_shard_step(const cbx_batch* b, const double* matrix, int64_t ld_m
   ShardArgs sa{own_lo, own_hi, first, xchg, step_state};
   return launch_params(b, matrix, ld_matrix, run, 1, 0x7FFFFFFF, bounds_lo, bounds_hi, warm_cells, state, state_bytes,
                        topk, max_k, trace_i, trace_t, trace_v, out, stream, &sa);
+}
+
+int cbx_bandit_prewarm(const cbx_batch* b, const cbx_bandit_run_desc* runs, int64_t n_runs, const int64_t* warm_prefix,
+                       int64_t total_cells, const int32_t* warm_cells, int32_t* trace_i, int32_t* trace_t,
+                       double* trace_v, void* stream) {
+  if (n_runs <= 0 || total_cells <= 0) return CBX_OK;
+  if (!b || !runs || !warm_prefix || !trace_i || !trace_t || !trace_v)
+    return fail(CBX_EINVAL, "bandit prewarm: NULL buffer");
+  if (n_runs > 0x7FFFFFFF) return fail(CBX_EINVAL, "bandit prewarm: too many runs");
+  const size_t es = dtype_size(b->dtype);
+  if ((b->dim * es) % 16 != 0) return fail(CBX_EINVAL, "bandit: token rows must be a multiple of 16 bytes");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  warm_draw_kernel<<<(unsigned)((n_runs + 127) / 128), 128, 0, st>>>(runs, (int)n_runs, warm_cells, trace_i, trace_t);
+  CBX_LAUNCH_CHECK("warm_draw_kernel launch");
+  BanditParams P{};
+  P.q_tokens = b->q_tokens;
+  P.q_tok_off = b->q_tok_off;
+  P.d_tokens = b->d_tokens;
+  P.d_tok_off = b->d_tok_off;
+  P.dim = b->dim;
+  P.clamp_negative = b->clamp_negative;
+  P.runs = runs;
+  P.trace_i = trace_i;
+  P.trace_t = trace_t;
+  P.trace_v = trace_v;
+  const int64_t warps = std::min<int64_t>(total_cells, (int64_t)sm_count() * 8 * 4);
+  const unsigned grid = (unsigned)((warps + 7) / 8);
+  const int dt = b->dtype, dim = b->dim;
+  auto go = [&](auto kern) -> int {
+    kern<<<grid, 256, 0, st>>>(P, (int)n_runs, warm_prefix);
+    CBX_LAUNCH_CHECK("warm_cells_kernel launch");
+    return CBX_OK;
+  };
+  auto pick = [&](auto tag) -> int {
+    using T = decltype(tag);
+    constexpr int PER = 16 / sizeof(T);
+    const int nvec = dim / PER;
+    if (nvec <= 8) return go(warm_cells_kernel<T, 8, 1>);
+    if (nvec <= 16) return go(warm_cells_kernel<T, 16, 1>);
+    if (nvec <= 32) return go(warm_cells_kernel<T, 32, 1>);
+    if (nvec <= 64) return go(warm_cells_kernel<T, 32, 2>);
+    if (nvec <= 128) return go(warm_cells_kernel<T, 32, 4>);
+    return fail(CBX_EINVAL, "bandit: embedding rows above 2 KiB are not supported");
+  };
+  switch (dt) {
+    case CBX_F32: return pick(float());
+    case CBX_F16: return pick(__half());
+    case CBX_BF16: return pick(__nv_bfloat16());
+    case CBX_F64: return pick(double());
+  }
+  return fail(CBX_EINVAL, "bandit prewarm: unknown dtype");
 }
 
 }  // extern "C"

@@ -11,7 +11,7 @@ import torch  # noqa: E402
 
 from paper_2602_02827_b200 import BanditConfig, BanditJob, run_batch  # noqa: E402
 from paper_2602_02827_b200 import workloads as W  # noqa: E402
-from paper_2602_02827_b200.bandit import collect  # noqa: E402
+from paper_2602_02827_b200.bandit import collect, launch_batch, prepare_batch  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg2")
@@ -19,6 +19,8 @@ ap.add_argument("--queries", type=int, default=None)
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--phases", action="store_true")
 ap.add_argument("--selection", default="auto")
+ap.add_argument("--no-prewarm", action="store_true")
+ap.add_argument("--prewarm", action="store_true")
 ap.add_argument("--runs", type=int, default=None, help="runs over the first --queries queries, round robin (footprint test)")
 a = ap.parse_args()
 cfg = W.CONFIGS[a.config]
@@ -40,14 +42,16 @@ if a.phases:
 elem = b.d_tokens.element_size()
 for it in range(a.iters):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prep = prepare_batch(jobs, batch=b, prewarm=False if a.no_prewarm else (True if a.prewarm else None))
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     e0.record()
-    raw = run_batch(jobs, batch=b, sync=False)
+    raw = launch_batch(prep)
     e1.record()
     torch.cuda.synchronize()
     host = time.perf_counter() - t0
     ms = e0.elapsed_time(e1)
-    res = collect(raw, jobs)
+    res = collect(raw, jobs, list(prep["results"]))
     reveals = sum(len(r.reveals) for r in res)
     iters = sum(r.iterations for r in res)
     gbytes = 0
