@@ -226,3 +226,24 @@ def test_tree_and_scan_selection_agree_with_the_oracle(selection):
                         batch=b)[0]
         ref = bandit_ref.run(cells, -1.0, 1.0, k, seed=(0, 7))
         assert res.reveals == ref.reveals and res.topk == ref.topk and res.iterations == ref.iterations
+
+
+def test_prewarm_pre_pass_gives_identical_runs():
+    """cbx_bandit_prewarm (grid-wide warm-up cells ahead of the loop kernel) must not change any trace."""
+    from paper_2602_02827_b200 import BanditConfig, BanditJob, CellBounds, run_batch
+    from paper_2602_02827_b200.batch import TokenBatch
+
+    cases = [W.gen_query("cfg2", q, n_docs=150) for q in range(3)]
+    b = TokenBatch.from_host([c.query for c in cases], [case_doc_list(c) for c in cases])
+    cells = maxsim_ref.cell_matrix(cases[2].query64(), cases[2].docs64())
+    rng = np.random.default_rng(2)
+    tight = CellBounds(cells - rng.uniform(0, 0.2, cells.shape), cells + rng.uniform(0, 0.2, cells.shape))
+    jobs = [BanditJob(BanditConfig(k=5, seed=(0, 0)), 150, 32, 0, 0),
+            BanditJob(BanditConfig(k=5, seed=(0, 1), explore_mode="static-warmup", gamma_init=0.1), 150, 32, 1, 150),
+            BanditJob(BanditConfig(k=5, seed=(0, 2)), 150, 32, 2, 300, tight)]
+    a = run_batch(jobs, batch=b, prewarm=True)
+    c = run_batch(jobs, batch=b, prewarm=False)
+    for x, y in zip(a, c):
+        assert x.reveals == y.reveals and x.topk == y.topk and x.iterations == y.iterations
+    ref = bandit_ref.run(cells, tight.lo, tight.hi, 5, seed=(0, 2))
+    assert [tuple(r) for r in a[2].reveals] == [tuple(r) for r in ref.reveals]
