@@ -748,7 +748,8 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
   };
 
   // ledger._record (oracle.py:305-314) + refresh(i) (bandit.py:220-247) for one row
-  auto reveal_update = [&](int i, int t, double v) -> bool {
+  // pre: the two unrevealed-bound sums after removing column t, already computed (per-cell bounds)
+  auto reveal_update = [&](int i, int t, double v, const double* pre = nullptr) -> bool {
     const int n = rv.cnt[i] + 1;
     double mean = rv.mean[i], m2 = rv.m2[i];
     BD_PHASE(8);
@@ -768,6 +769,9 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       // fsum of (T - n) copies of a constant == the correctly rounded product
       lo_sum = (TC - n) ? __dmul_rn((double)(TC - n), R.lo_uniform) : 0.0;
       hi_sum = (TC - n) ? __dmul_rn((double)(TC - n), R.hi_uniform) : 0.0;
+    } else if (pre) {
+      lo_sum = pre[0];
+      hi_sum = pre[1];
     } else {
       ok &= exp_add(&g_lo[i], -lo_b[(int64_t)i * TC + t], &lo_sum);
       ok &= exp_add(&g_hi[i], -hi_b[(int64_t)i * TC + t], &hi_sum);
@@ -963,6 +967,8 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
     }
     BD_PHASE(0);
     if (warp == 0) {
+      int wsel_i = -1;
+      uint64_t wsel_un = 0;
       Cand f[4];
       if (use_tree) {
 #pragma unroll
@@ -1012,18 +1018,10 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
             } else if (uniform) {
               t_star = __ffsll((long long)un) - 1;  // all widths equal: first unrevealed column
             } else {
-              // first argmax of the width over the ascending unrevealed columns
-              double best = -INFINITY;
+              // first argmax of the width over the ascending unrevealed columns: warp 0 below
               t_star = -1;
-              for (int t = 0; t < TC; ++t) {
-                if (!((un >> t) & 1ull)) continue;
-                const double w = __dsub_rn(hi_b[(int64_t)i_star * TC + t], lo_b[(int64_t)i_star * TC + t]);
-                if (w > best) {
-                  best = w;
-                  t_star = t;
-                }
-              }
-              if (t_star < 0) t_star = __ffsll((long long)un) - 1;
+              wsel_i = i_star;
+              wsel_un = un;
             }
             ctrl->i_star = i_star;
             ctrl->t_star = t_star;
@@ -1031,6 +1029,16 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
           }
         }
         ctrl->action = action;
+      }
+      const int wi = __shfl_sync(0xffffffffu, wsel_i, 0);
+      if (wi >= 0) {  // one column per lane, warp argmax, ties to the lowest column (select_token, bandit.py:116-136)
+        const uint64_t un = __shfl_sync(0xffffffffu, wsel_un, 0);
+        Cand c{0, TIE_EMPTY};
+        for (int t = lane; t < TC; t += 32)
+          if ((un >> t) & 1ull)
+            cand_take(c, ord_key(__dsub_rn(hi_b[(int64_t)wi * TC + t], lo_b[(int64_t)wi * TC + t])), (uint32_t)t);
+        c = warp_best(c);
+        if (lane == 0) ctrl->t_star = c.key ? (int)c.tie : __ffsll((long long)un) - 1;
       }
     }
     __syncthreads();
@@ -1128,6 +1136,16 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
     }
     BD_PHASE(2);
     int partner = -1;
+    double pre[2] = {0.0, 0.0};
+    if (!uniform && warp == 0 && lane < 2) {
+      // the exact unrevealed-bound sums of lo (lane 0) and hi (lane 1) at once
+      double r;
+      if (!exp_add(lane == 0 ? &g_lo[i_star] : &g_hi[i_star], -(lane == 0 ? lo_b : hi_b)[(int64_t)i_star * TC + t_star],
+                   &r))
+        ctrl->status = 2;
+      pre[0] = r;
+      pre[1] = __shfl_sync(0x3u, r, 1);
+    }
     if (tid == 0) {
       const double v = (tokens || P.shard) ? ord_val(ctrl->cellkey)
                                            : P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
@@ -1136,7 +1154,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       tr_t[pos] = t_star;
       tr_v[pos] = v;
       ctrl->n_reveals = pos + 1;
-      if (!reveal_update(i_star, t_star, v)) ctrl->status = 2;
+      if (!reveal_update(i_star, t_star, v, uniform ? nullptr : pre)) ctrl->status = 2;
       // keep the Top-K set equal to the first K of the (-proxy, i) order
       const uint64_t mk = ord_key(rv.proxy[i_star]);
       if (rv.member[i_star]) {
