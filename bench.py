@@ -321,23 +321,28 @@ def run_ours(args, rank, world, local_rank):
         del hb
 
     # ------------------------------------------------ P2: the Col-Bandit loop on the same batch
+    # the sections below are reported beside the headline; a failure in one is recorded, not fatal
+    # (every rank runs the same code on the same shapes, so a failure is symmetric across ranks)
+    def section(name, fn):
+        try:
+            out = fn()
+        except Exception as e:  # noqa: BLE001
+            out = {"error": f"{type(e).__name__}: {e}"[:500]}
+            print(f"bench: section {name} failed: {out['error']}", file=sys.stderr, flush=True)
+        if rank == 0:
+            result[name] = out
+
     if not args.no_bandit:
-        bandit = run_bandit(args, batch, host_off, cfg, rank, world)
-        if rank == 0:
-            result["bandit"] = bandit
+        section("bandit", lambda: run_bandit(args, batch, host_off, cfg, rank, world))
     # ------------------------------------------------ Stage 1 (candidate scan) + the reranker facade, cfg4 corpus
+    del batch
+    torch.cuda.empty_cache()
     if not args.no_stage1:
-        del batch
-        torch.cuda.empty_cache()
-        s1 = run_stage1(args, rank, world)
-        if rank == 0:
-            result["stage1"] = s1
+        section("stage1", lambda: run_stage1(args, rank, world))
     # ------------------------------------------------ P2 document-sharded over the ranks (cfg4)
     if not args.no_p2_sharded:
         torch.cuda.empty_cache()
-        ps = run_p2_sharded(args, rank, world)
-        if rank == 0:
-            result["bandit_sharded"] = ps
+        section("bandit_sharded", lambda: run_p2_sharded(args, rank, world))
     if rank == 0:
         print(json.dumps(result), flush=True)
 
