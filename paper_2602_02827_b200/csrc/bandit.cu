@@ -658,8 +658,12 @@ __device__ __forceinline__ double tokens_max(const T* __restrict__ dtok, int64_t
 }
 
 // ----------------------------------------------------------------- the kernel
-template <typename T, int G, int VPL>
-__global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParams P) {
+template <typename T, int G, int VPL, int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const BanditParams P) {
+  // NT = 256: two runs per SM (register file split); NT = 512 when every run has an SM to itself:
+  // twice the warps for the reveal and the warm-up of one run
+  constexpr int BD_THREADS = NT;
+  constexpr int BD_WARPS = NT / 32;
   extern __shared__ __align__(16) uint8_t bd_smem[];
   constexpr int NGROUPS = BD_THREADS / G;
 #ifndef CBX_BD_TOKENS_IN_FLIGHT
@@ -690,7 +694,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
   };
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(bd_smem);
   Cand* red = reinterpret_cast<Cand*>(bd_smem + 128);                 // [4][BD_WARPS]
-  double* sq_log = reinterpret_cast<double*>(red + 4 * BD_WARPS);     // [BD_MAX_T + 1]
+  double* sq_log = reinterpret_cast<double*>(red + 4 * 16);           // [BD_MAX_T + 1]
   double* sq_rho = sq_log + BD_MAX_T + 1;                             // [BD_MAX_T + 1]
   uint8_t* row_base = reinterpret_cast<uint8_t*>(sq_rho + BD_MAX_T + 1);
   if (!P.use_smem) row_base = P.g_rows + (size_t)R.state_off * ROW_STRIDE;
@@ -749,7 +753,8 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
 
   // ledger._record (oracle.py:305-314) + refresh(i) (bandit.py:220-247) for one row
   // pre: the two unrevealed-bound sums after removing column t, already computed (per-cell bounds)
-  auto reveal_update = [&](int i, int t, double v, const double* pre = nullptr) -> bool {
+  auto reveal_update = [&](int i, int t, double v, bool have_pre = false, double pre_lo = 0.0,
+                           double pre_hi = 0.0) -> bool {
     const int n = rv.cnt[i] + 1;
     double mean = rv.mean[i], m2 = rv.m2[i];
     BD_PHASE(8);
@@ -769,9 +774,9 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       // fsum of (T - n) copies of a constant == the correctly rounded product
       lo_sum = (TC - n) ? __dmul_rn((double)(TC - n), R.lo_uniform) : 0.0;
       hi_sum = (TC - n) ? __dmul_rn((double)(TC - n), R.hi_uniform) : 0.0;
-    } else if (pre) {
-      lo_sum = pre[0];
-      hi_sum = pre[1];
+    } else if (have_pre) {
+      lo_sum = pre_lo;
+      hi_sum = pre_hi;
     } else {
       ok &= exp_add(&g_lo[i], -lo_b[(int64_t)i * TC + t], &lo_sum);
       ok &= exp_add(&g_hi[i], -hi_b[(int64_t)i * TC + t], &hi_sum);
@@ -1030,7 +1035,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
         }
         ctrl->action = action;
       }
-      const int wi = __shfl_sync(0xffffffffu, wsel_i, 0);
+      const int wi = uniform ? -1 : __shfl_sync(0xffffffffu, wsel_i, 0);
       if (wi >= 0) {  // one column per lane, warp argmax, ties to the lowest column (select_token, bandit.py:116-136)
         const uint64_t un = __shfl_sync(0xffffffffu, wsel_un, 0);
         Cand c{0, TIE_EMPTY};
@@ -1136,15 +1141,15 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
     }
     BD_PHASE(2);
     int partner = -1;
-    double pre[2] = {0.0, 0.0};
+    double pre_lo = 0.0, pre_hi = 0.0;
     if (!uniform && warp == 0 && lane < 2) {
       // the exact unrevealed-bound sums of lo (lane 0) and hi (lane 1) at once
       double r;
       if (!exp_add(lane == 0 ? &g_lo[i_star] : &g_hi[i_star], -(lane == 0 ? lo_b : hi_b)[(int64_t)i_star * TC + t_star],
                    &r))
         ctrl->status = 2;
-      pre[0] = r;
-      pre[1] = __shfl_sync(0x3u, r, 1);
+      pre_lo = r;
+      pre_hi = __shfl_sync(0x3u, r, 1);
     }
     if (tid == 0) {
       const double v = (tokens || P.shard) ? ord_val(ctrl->cellkey)
@@ -1154,7 +1159,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2) bandit_kernel(const BanditParam
       tr_t[pos] = t_star;
       tr_v[pos] = v;
       ctrl->n_reveals = pos + 1;
-      if (!reveal_update(i_star, t_star, v, uniform ? nullptr : pre)) ctrl->status = 2;
+      if (!reveal_update(i_star, t_star, v, !uniform, pre_lo, pre_hi)) ctrl->status = 2;
       // keep the Top-K set equal to the first K of the (-proxy, i) order
       const uint64_t mk = ord_key(rv.proxy[i_star]);
       if (rv.member[i_star]) {
@@ -1336,11 +1341,15 @@ static size_t state_parts(int64_t rows, size_t* off_obs, size_t* off_lo, size_t*
   return o;
 }
 
+#ifndef CBX_BD_WIDE
+#define CBX_BD_WIDE 1  // 512-thread CTAs when the runs fit one per SM
+#endif
 template <typename T, int G, int VPL>
 static int launch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, cudaStream_t st) {
-  auto kern = bandit_kernel<T, G, VPL>;
+  const bool wide = CBX_BD_WIDE && n_runs <= sm_count();
+  auto kern = wide ? bandit_kernel<T, G, VPL, 512> : bandit_kernel<T, G, VPL, 256>;
   CBX_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<(unsigned)n_runs, BD_THREADS, smem, st>>>(P);
+  kern<<<(unsigned)n_runs, wide ? 512 : 256, smem, st>>>(P);
   CBX_LAUNCH_CHECK("bandit_kernel launch");
   return CBX_OK;
 }
@@ -1511,7 +1520,7 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
   P.own_hi = sa ? sa->own_hi : 0;
   P.xchg = sa ? sa->xchg : nullptr;
   P.step = sa ? static_cast<BdStep*>(sa->step) : nullptr;
-  size_t smem = 128 + sizeof(Cand) * 4 * BD_WARPS + 2 * sizeof(double) * (BD_MAX_T + 1);
+  size_t smem = 128 + sizeof(Cand) * 4 * 16 + 2 * sizeof(double) * (BD_MAX_T + 1);  // reductions: up to 16 warps
   smem = align_up(smem, 16);
   P.use_smem = (max_rows <= BD_SMEM_ROWS && !sa) ? 1 : 0;  // a sharded run resumes from global state
   if (P.use_smem) smem += (size_t)(max_rows + BD_ROW_SLACK) * ROW_STRIDE + 64;
