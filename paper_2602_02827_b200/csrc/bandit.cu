@@ -98,6 +98,7 @@ struct BanditParams {
   ExpStore* g_hi;      // [rows]
   uint8_t* g_rows;     // [rows * ROW_BYTES] per-row state when it does not fit in smem
   int use_smem;
+  int trees_smem;      // rows global, selection trees in shared memory (set by the host when they fit)
   int32_t* topk;
   int32_t max_k;
   int32_t* trace_i;
@@ -702,7 +703,10 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
   rv.carve(row_base, N);
   const bool use_tree = (R.flags & CBX_BANDIT_TREE) != 0;
   Trees tr;
-  tr.carve(row_base + align_up_dev(ROW_BYTES * (size_t)N, 16), N);
+  // trees in shared memory when the rows are in global memory but the CTA has the SM to itself
+  // (one run per SM: decide and the per-level tree walks become shared-memory round trips)
+  tr.carve(P.trees_smem ? reinterpret_cast<uint8_t*>(sq_rho + BD_MAX_T + 1)
+                        : row_base + align_up_dev(ROW_BYTES * (size_t)N, 16), N);
   ExpStore* g_obs = P.g_obs + R.state_off;
   ExpStore* g_lo = P.g_lo + R.state_off;
   ExpStore* g_hi = P.g_hi + R.state_off;
@@ -989,8 +993,13 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
         ctrl->swap_out = f[3].key ? (int)~f[3].tie : -1;
         const int i_plus = (int)f[0].tie;
         const int i_minus = f[1].key ? (int)f[1].tie : -1;
-        const double lcb_plus = rv.lcb[i_plus];
-        const double ucb_minus = i_minus >= 0 ? rv.ucb[i_minus] : -INFINITY;
+        const int im = i_minus >= 0 ? i_minus : i_plus;  // a valid row for the loads below
+        // the selection keys carry the bounds (key 0 = ~ord(lcb) over members, key 1 = ord(ucb) over the rest)
+        const double lcb_plus = ord_val(~f[0].key);
+        const double ucb_minus = i_minus >= 0 ? ord_val(f[1].key) : -INFINITY;
+        // everything else the decision may read, issued together (one round trip when rows live in HBM)
+        const double ucb_p = rv.ucb[i_plus], lcb_m = rv.lcb[im];
+        const uint64_t un_p = rv.unrev[i_plus], un_m = rv.unrev[im];
         int action;
         if (lcb_plus >= ucb_minus) {
           action = 1;
@@ -1001,13 +1010,13 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
           action = 3;
         } else {
           action = 0;
-          const double wp = __dsub_rn(rv.ucb[i_plus], lcb_plus);
-          const double wm = __dsub_rn(ucb_minus, rv.lcb[i_minus]);
+          const double wp = __dsub_rn(ucb_p, lcb_plus);
+          const double wm = __dsub_rn(ucb_minus, lcb_m);
           int i_star = wp >= wm ? i_plus : i_minus;
-          uint64_t un = rv.unrev[i_star];
+          uint64_t un = i_star == i_plus ? un_p : un_m;
           if (!un) {
             i_star = i_star == i_plus ? i_minus : i_plus;
-            un = rv.unrev[i_star];
+            un = i_star == i_plus ? un_p : un_m;
             if (!un) {
               action = 4;
               ctrl->status = 1;
@@ -1524,6 +1533,21 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
   smem = align_up(smem, 16);
   P.use_smem = (max_rows <= BD_SMEM_ROWS && !sa) ? 1 : 0;  // a sharded run resumes from global state
   if (P.use_smem) smem += (size_t)(max_rows + BD_ROW_SLACK) * ROW_STRIDE + 64;
+  P.trees_smem = 0;
+  if (!P.use_smem && !sa && CBX_BD_WIDE && n_runs <= sm_count()) {
+    // 4 trees x (8-byte key + 4-byte tie) per node; nodes = sum over 32-ary levels
+    int64_t nn = 0, sz = ((int64_t)max_rows + 31) / 32;
+    for (int l = 0; l < 8; ++l) {
+      nn += sz;
+      if (sz == 1) break;
+      sz = (sz + 31) / 32;
+    }
+    const size_t tb = align_up((size_t)nn * 4 * 12, 16);
+    if (smem + tb <= 220 * 1024) {
+      P.trees_smem = 1;
+      smem += tb;
+    }
+  }
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int dt = b ? b->dtype : CBX_F64;
