@@ -87,7 +87,7 @@ for name in a.configs.split(","):
                     "p2_gather_gbs": gather / bms / 1e6, "p2_gather_frac": gather / bms / 1e6 / peak,
                     "p2_coverage_mean": float(np.mean(cov)), "p2_iterations": int(sum(r.iterations for r in res))})
         if cfg.n_docs <= 5000:
-            same = True
+            same = crit = True
             for ji in range(min(a.check * len(cfg.alphas), len(jobs))):
                 j = jobs[ji]
                 q = j.query
@@ -98,7 +98,9 @@ for name in a.configs.split(","):
                 cm = maxsim_ref.cell_matrix(qt, docs)
                 ref = bandit_ref.run(cm, -1.0, 1.0, cfg.k, alpha_ef=j.cfg.alpha_ef, seed=(0, q))
                 same &= ref.reveals == res[ji].reveals and ref.topk == res[ji].topk
+                crit &= set(ref.topk) == set(res[ji].topk) and abs(ref.coverage - res[ji].coverage) <= 0.02
             out["p2_trace_parity"] = same
+            out["p2_baseline_criterion"] = crit  # same Top-K set, coverage within 2 % (BASELINE north star)
     # the reference algorithm on one host core (oracle port, BLAS 1 thread), a time-bounded query sample
     if a.cpu_seconds > 0:
         os.environ["OPENBLAS_NUM_THREADS"] = "1"
