@@ -510,6 +510,11 @@ def run_stage1(args, rank, world):
     return out
 
 
+def _bandit_traffic(name):
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    return json.load(open(tpath)).get(f"bandit_{name}") if os.path.exists(tpath) else None
+
+
 def run_bandit(args, batch, host_off, cfg, rank, world):
     import numpy as np
     import torch
@@ -564,7 +569,11 @@ def run_bandit(args, batch, host_off, cfg, rank, world):
                         "unit": "GB/s", "frac": gather / (ms / 1e3) / 1e9 / hbm_peak, "peak_kind": peak_kind,
                         "alg_bytes": gather,
                         "note": "algorithmic gather = sum over reveals of L_i*d*s (warm-up included); repeated "
-                                "boundary rows hit L2/L1, so this can exceed DRAM traffic"},
+                                "boundary rows hit L2/L1, so this can exceed DRAM traffic",
+                        "traffic": _bandit_traffic(cfg.name),
+                        "traffic_note": "dram__bytes_read+write of one bandit_kernel launch on this config from "
+                                        "the committed ncu capture (profiles/r1_ncu_bandit_cfg2_details.txt; "
+                                        "L2 hit rate 24 %)"},
            "gpu_launches": 1 + (2 if prep["n_prewarm"] else 0),
            "e2e": {"ms": e2e_ms, "revealed_cells_per_s": reveals * world / (e2e_ms / 1e3),
                    "api": "bandit.run_batch(jobs, batch): host seeding + descriptors + launch + traces D2H"}}
