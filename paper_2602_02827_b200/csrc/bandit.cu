@@ -99,6 +99,8 @@ struct BanditParams {
   uint8_t* g_rows;     // [rows * ROW_BYTES] per-row state when it does not fit in smem
   int use_smem;
   int trees_smem;      // rows global, selection trees in shared memory (set by the host when they fit)
+  int bounds_smem;     // expansions (+ per-cell bounds) in shared memory at byte offset bounds_smem_off
+  int64_t bounds_smem_off;
   int32_t* topk;
   int32_t max_k;
   int32_t* trace_i;
@@ -379,7 +381,31 @@ __device__ __noinline__ bool exp_leave_grid(ExpStore* st, long long f, double v)
   store_exp(*st, e);
   return ok;
 }
+// A store with n == -1 holds an exact int64 fixed-point sum (x 2^48) in p[0]: exp_init picks it when every
+// value lies on the 2^-48 grid (per-cell bounds derived from fp16 tokens always do), and then a bound update
+// is an integer add and one correctly rounded conversion instead of an expansion pass.
+__device__ __forceinline__ double fixed_value(long long f) { return __dmul_rn(__ll2double_rn(f), BD_FX_INV); }
 __device__ __noinline__ bool exp_add(ExpStore* st, double v, double* rounded) {
+  if (st->n == -1) {
+    long long q;
+    const long long f = __double_as_longlong(st->p[0]);
+    if (to_fixed(v, q)) {
+      st->p[0] = __longlong_as_double(f + q);
+      if (rounded) *rounded = fixed_value(f + q);
+      return true;
+    }
+    // off the grid after all: continue as an expansion (exact two-term split of the integer sum)
+    const double hi = __ll2double_rn(f);
+    const double lo = __ll2double_rn(f - __double2ll_rn(hi));
+    Expansion<BD_CAP> e;
+    e.clear();
+    bool ok = e.add(__dmul_rn(lo, BD_FX_INV));
+    ok &= e.add(__dmul_rn(hi, BD_FX_INV));
+    ok &= e.add(v);
+    store_exp(*st, e);
+    if (rounded) *rounded = e.round();
+    return ok;
+  }
   Expansion<BD_CAP> e;
   load_exp(e, *st);
   const bool ok = e.add(v);
@@ -393,6 +419,19 @@ __device__ __noinline__ double exp_value(const ExpStore* st) {
   return e.round();
 }
 __device__ __noinline__ bool exp_init(ExpStore* st, const double* vals, int n, double* rounded) {
+  long long f = 0;
+  bool grid = true;
+  for (int t = 0; t < n && grid; ++t) {
+    long long q;
+    grid = to_fixed(vals[t], q);
+    f += q;
+  }
+  if (grid) {
+    st->p[0] = __longlong_as_double(f);
+    st->n = -1;
+    *rounded = fixed_value(f);
+    return true;
+  }
   Expansion<BD_CAP> e;
   e.clear();
   bool ok = true;
@@ -710,6 +749,25 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
   ExpStore* g_obs = P.g_obs + R.state_off;
   ExpStore* g_lo = P.g_lo + R.state_off;
   ExpStore* g_hi = P.g_hi + R.state_off;
+  if (P.bounds_smem) {
+    // one run per SM and a small pool: the exact-sum expansions and the per-cell bounds are staged in
+    // shared memory, so the greedy column choice and the interval updates stop paying HBM round trips
+    ExpStore* se = reinterpret_cast<ExpStore*>(bd_smem + P.bounds_smem_off);
+    g_obs = se;
+    g_lo = se + N;
+    g_hi = se + 2 * N;
+    if (!uniform) {
+      double* slo = reinterpret_cast<double*>(se + 3 * N);
+      double* shi = slo + (size_t)N * TC;
+      for (int64_t x = tid; x < (int64_t)N * TC; x += BD_THREADS) {
+        slo[x] = lo_b[x];
+        shi[x] = hi_b[x];
+      }
+      lo_b = slo;
+      hi_b = shi;
+    }
+    __syncthreads();
+  }
   int32_t* tr_i = P.trace_i + R.trace_off;
   int32_t* tr_t = P.trace_t + R.trace_off;
   double* tr_v = P.trace_v + R.trace_off;
@@ -729,7 +787,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
   unsigned long long tc0 = clock64();
 #define BD_PHASE(k)                            \
   do {                                         \
-    if (P.prof && tid == 0) {                  \
+    if (__builtin_expect(P.prof != nullptr, 0) && tid == 0) { \
       const unsigned long long _n = clock64(); \
       ph[k] += _n - tc0;                       \
       tc0 = _n;                                \
@@ -737,14 +795,14 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
   } while (0)
   // exact sum of a row's revealed values, rounded like math.fsum
   auto obs_sum = [&](int i) -> double {
-    if (rv.exp_mode[i]) return exp_value(&g_obs[i]);
+    if (__builtin_expect(rv.exp_mode[i], 0)) return exp_value(&g_obs[i]);
     return __dmul_rn(__ll2double_rn(rv.fx[i]), BD_FX_INV);
   };
   // add v to row i's exact sum; false on expansion overflow
   auto obs_add = [&](int i, double v) -> bool {
     long long q;
-    if (!rv.exp_mode[i]) {
-      if (to_fixed(v, q)) {
+    if (__builtin_expect(!rv.exp_mode[i], 1)) {
+      if (__builtin_expect(to_fixed(v, q), 1)) {
         rv.fx[i] += q;
         return true;
       }
@@ -953,9 +1011,9 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
   while (true) {
     BD_PHASE(3);
     int i_star, t_star;
-    if (resume_kind == 0) {
+    if (__builtin_expect(resume_kind == 0, 1)) {
     // ---------------------------------------------------------- boundary selection
-    if (!use_tree) {
+    if (__builtin_expect(!use_tree, 0)) {
       Cand c[4] = {{0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}, {0, TIE_EMPTY}};
       for (int i = tid; i < N; i += BD_THREADS) {
         const uint64_t pk = ord_key(rv.proxy[i]);
@@ -1065,7 +1123,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
     }
     if (action == 4) break;
 
-    if (action == 2) {
+    if (__builtin_expect(action == 2, 0)) {
       // -------------------------------------------------------- lazy warm-up (bandit.py:285-296)
       warmed = true;
       const int64_t base = ctrl->n_reveals;
@@ -1124,7 +1182,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
       if (lane == 0) atomicMax(&ctrl->cellkey, (unsigned long long)ord_key(best));
       __syncthreads();
     }
-    if (P.shard) {
+    if (__builtin_expect(P.shard, 0)) {
       if (tid == 0) {
         const double v = tokens ? ord_val(ctrl->cellkey) : P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
         P.xchg[0] = own ? xchg_key(ord_key(v)) : INT64_MIN;
@@ -1546,6 +1604,19 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
     if (smem + tb <= 220 * 1024) {
       P.trees_smem = 1;
       smem += tb;
+    }
+  }
+  P.bounds_smem = 0;
+  P.bounds_smem_off = 0;
+  if (!sa && CBX_BD_WIDE && n_runs <= sm_count() && max_rows <= BD_SMEM_ROWS) {
+    // 3 expansions per row, plus lo/hi for up to BD_MAX_T columns per row when per-cell bounds are given
+    const size_t need = (size_t)max_rows * 3 * sizeof(ExpStore) +
+                        (bounds_lo ? (size_t)max_rows * BD_MAX_T * 2 * sizeof(double) : 0);
+    const size_t off = align_up(smem, 16);
+    if (off + need <= 220 * 1024) {
+      P.bounds_smem = 1;
+      P.bounds_smem_off = (int64_t)off;
+      smem = off + need;
     }
   }
 
