@@ -64,3 +64,14 @@ def test_error_mapping():
         _lib.check(_lib.CBX_ERANGE)
     with pytest.raises(RuntimeError):
         _lib.check(_lib.CBX_EINTERNAL)
+
+
+def test_product_package_never_imports_the_test_oracle():
+    """The CPU restatement under oracle/ is the checker only: no module of the product may import it
+    (``paper_2602_02827_b200.oracle`` is the package's own device-backed MaxSimOracle, imported relatively)."""
+    pkg = os.path.join(ROOT, "paper_2602_02827_b200")
+    for name in sorted(os.listdir(pkg)):
+        if not name.endswith(".py"):
+            continue
+        src = open(os.path.join(pkg, name)).read()
+        assert not re.search(r"^\s*(from\s+oracle\b|import\s+oracle\b)", src, flags=re.M), name
