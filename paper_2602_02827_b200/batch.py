@@ -437,10 +437,12 @@ class Corpus:
         if cid.numel() != n_cand:
             raise ValueError("cand_ids length does not match q_cand_off[-1]")
         cid_np = cid.numpy()
-        if n_cand and (cid_np.min() < 0 or cid_np.max() >= self.n_docs):
-            raise IndexError(f"candidate id out of range [0, {self.n_docs})")
         if mode not in ("packed", "gather"):
             raise ValueError(f"mode must be 'packed' or 'gather', got {mode!r}")
+        # packed mode checks the ids on the device (a bad id scores as an empty document and raises
+        # IndexError at the synchronisation below); the gather mode sizes its copy on the host
+        if mode == "gather" and n_cand and (cid_np.min() < 0 or cid_np.max() >= self.n_docs):
+            raise IndexError(f"candidate id out of range [0, {self.n_docs})")
         # host -> device: the call's inputs only
         dq = self._buf("q", q_tokens.numel(), q_tokens.dtype).view(q_tokens.shape)
         dq.copy_(q_tokens, non_blocking=True)
