@@ -490,8 +490,10 @@ class Corpus:
         out_v = self._buf("ov", val.numel(), torch.float32, pinned=True).view(val.shape)
         out_i.copy_(idx, non_blocking=True)
         out_v.copy_(val, non_blocking=True)
+        st_h = self._buf("st_h", 1, torch.int32, pinned=True)
+        st_h.copy_(status, non_blocking=True)  # read back with the outputs: one synchronisation per call
         if sync:
             torch.cuda.current_stream().synchronize()
-            if int(status.item()):
+            if int(st_h[0]):
                 raise IndexError("candidate id out of range")
         return out_i, out_v
