@@ -55,7 +55,6 @@ struct RowsView {
   double* m2;          // Welford sum of squared deviations
   long long* fx;       // exact sum of revealed values x 2^48 while every value is on that grid
   uint64_t* unrev;     // bit t set = column t not yet revealed
-  uint64_t* wkey;      // warm-up scratch: ordered key of the row's warm-up cell
   int32_t* cnt;        // revealed cells per row
   uint8_t* exp_mode;   // 1: the row's exact sum lives in the global expansion store
   uint8_t* member;     // Top-K membership
@@ -67,13 +66,12 @@ struct RowsView {
     m2 = mean + N;
     fx = reinterpret_cast<long long*>(m2 + N);
     unrev = reinterpret_cast<uint64_t*>(fx + N);
-    wkey = unrev + N;
-    cnt = reinterpret_cast<int32_t*>(wkey + N);
+    cnt = reinterpret_cast<int32_t*>(unrev + N);
     exp_mode = reinterpret_cast<uint8_t*>(cnt + N);
     member = exp_mode + N;
   }
 };
-constexpr size_t ROW_BYTES = 8 * 8 + 4 + 1 + 1;
+constexpr size_t ROW_BYTES = 7 * 8 + 4 + 1 + 1;
 // tournament-tree nodes get 4 bytes per row (+ CBX_BANDIT_ROW_SLACK rows of slack per run)
 constexpr size_t ROW_STRIDE = ROW_BYTES + 4;
 constexpr int BD_ROW_SLACK = 64;
