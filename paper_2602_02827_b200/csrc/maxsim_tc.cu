@@ -51,6 +51,11 @@ struct TcParams {
   const int64_t* src_row;
   const int32_t* doc_len;
   const int64_t* n_tokens_dev;  // packed mode: total packed rows (d_tok_off[n_docs]) read on the device
+  // packed mode with dim % 64 == 0: stages interleave the K blocks per 8-row group so one 4-D TMA box
+  // carries all K blocks of a row range (TmapSet::pk); corpus_rows bounds those maps, k8 = 8-row 2-D map
+  int32_t ilv;
+  int32_t k8;
+  int64_t corpus_rows;
   int64_t n_queries;
   int64_t n_docs;
   int64_t n_tokens;      // total document tokens (partitioned evenly over the CTAs)
@@ -157,9 +162,13 @@ __device__ __forceinline__ float masked_max(const float (&v)[32], int s, int e, 
 
 // tensor maps: doc tiles of box heights tile_n >> k (k = 0..4; packed mode uses all of them to lay
 // documents out at 8-row granularity) and the query rows
+// pk[k][r]: packed interleaved mode, 4-D view {64 cols, 8 rows, kblocks, 8-row groups} of the corpus
+// from row r on, boxes of (tile_n >> k) rows x every K block
+static_assert(TC_PACK >= 32, "interleaved packed maps cover box heights tile_n >> {0,1,2} only");
 struct TmapSet {
   CUtensorMap d[5];
   CUtensorMap q;
+  CUtensorMap pk[3][8];
 };
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -283,9 +292,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int h = p.tile_n >> k;
                 if (h < TC_PACK) break;
                 while (ov1 - row >= h) {
-                  for (int kb = 0; kb < p.kblocks; ++kb)
-                    ptx::tma_load_2d_hint(dst + kb * p.tile_n * 128 + (row - r0) * 128, &tm.d[k], &full[stage],
-                                          kb * 64, (int32_t)srow, pol);
+                  if (p.ilv) {
+                    // interleaved stage: 8-row groups of kblocks x 1 KB; one 4-D box (rows x all K blocks)
+                    // through the map whose base is corpus row (srow & 7), unless the box reaches past that
+                    // map's last whole 8-row group (corpus tail: 8-row 2-D boxes, zero-filled past the end)
+                    uint8_t* bdst = dst + (row - r0) * 128 * p.kblocks;
+                    const int ph = (int)(srow & 7);
+                    const int64_t g = srow >> 3;
+                    if (g + (h >> 3) <= ((p.corpus_rows - ph) >> 3)) {
+                      ptx::tma_load_4d_hint(bdst, &tm.pk[k][ph], &full[stage], 0, 0, 0, (int32_t)g, pol);
+                    } else {
+                      for (int gi = 0; gi < (h >> 3); ++gi)
+                        for (int kb = 0; kb < p.kblocks; ++kb)
+                          ptx::tma_load_2d_hint(bdst + (gi * p.kblocks + kb) * 1024, &tm.d[p.k8], &full[stage],
+                                                kb * 64, (int32_t)(srow + gi * 8), pol);
+                    }
+                  } else {
+                    for (int kb = 0; kb < p.kblocks; ++kb)
+                      ptx::tma_load_2d_hint(dst + kb * p.tile_n * 128 + (row - r0) * 128, &tm.d[k], &full[stage],
+                                            kb * 64, (int32_t)srow, pol);
+                  }
                   row += h;
                   srow += h;
                 }
@@ -318,8 +344,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const uint32_t b_addr = ptx::smem_u32(stages + (size_t)stage * p.stage_bytes);
           const uint32_t d_tmem = tmem_base + acc * TC_MAX_TILE_N;
           // descriptors advance by (byte offset >> 4) in their 14-bit start-address field
-          const uint64_t bd0 = ptx::smem_desc_sw128(b_addr);
-          const uint32_t bstep = (uint32_t)(p.tile_n * 128) >> 4;
+          // interleaved (packed) stages: K block kb is 1 KB into each 8-row group, groups kblocks KB apart
+          const uint64_t bd0 = ptx::smem_desc_sw128(b_addr, p.ilv ? (uint32_t)p.kblocks * 1024u : 1024u);
+          const uint32_t bstep = (uint32_t)(p.ilv ? 1024 : p.tile_n * 128) >> 4;
 #pragma unroll
           for (int kb = 0; kb < 8; ++kb) {
             if (kb >= p.kblocks) break;
@@ -527,6 +554,27 @@ int make_tmap(CUtensorMap* m, const void* base, int dtype, int64_t rows, int32_t
   return CBX_OK;
 }
 
+// Interleaved view of rows [r0, r0 + 8 * groups) of a [rows, dim] token matrix (dim % 64 == 0):
+// {64 cols, 8 rows, dim / 64 K blocks, groups}, one box = box_rows rows x every K block, landing in
+// shared memory as box_rows / 8 groups of (dim / 64) swizzled 1 KB blocks.
+static int make_tmap_ilv(CUtensorMap* m, const void* base, int dtype, int64_t r0, int64_t groups, int32_t dim,
+                         uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return fail(CBX_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const int32_t kb = dim / 64;
+  const uint8_t* p0 = static_cast<const uint8_t*>(base) + (size_t)r0 * dim * 2;
+  cuuint64_t dims[4] = {64, 8, (cuuint64_t)kb, (cuuint64_t)(groups > 0 ? groups : 1)};
+  cuuint64_t strides[3] = {(cuuint64_t)dim * 2, 128, (cuuint64_t)dim * 16};
+  cuuint32_t box[4] = {64, 8, (cuuint32_t)kb, box_rows / 8};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, dtype == CBX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                   const_cast<uint8_t*>(p0), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(CBX_ECUDA, "cuTensorMapEncodeTiled (interleaved) failed (code " + std::to_string((int)r) + ")");
+  return CBX_OK;
+}
+
 bool tc_supported(const cbx_batch* b) {
   return (b->dtype == CBX_F16 || b->dtype == CBX_BF16) && b->max_lq >= 1 && b->max_lq <= 128 && b->dim % 8 == 0 &&
          b->dim <= 512 && b->n_d_tokens < (int64_t(1) << 31) && b->n_q_tokens < (int64_t(1) << 31);
@@ -670,6 +718,9 @@ static int prepare_tc(const cbx_batch* b, const void* d_rows, int64_t n_rows, fl
   p.src_row = nullptr;
   p.doc_len = nullptr;
   p.n_tokens_dev = nullptr;
+  p.ilv = 0;
+  p.k8 = tile_n == 128 ? 4 : 2;  // d[k8] = 8-row boxes
+  p.corpus_rows = n_rows;
   p.n_queries = b->n_queries;
   p.n_docs = b->n_docs;
   p.n_tokens = b->n_d_tokens;
@@ -732,6 +783,17 @@ int launch_maxsim_tc_packed(const cbx_batch* b, const int64_t* corpus_off, int64
   int rc = prepare_tc(b, b->d_tokens, b->n_d_tokens, scores, L);
   if (rc) return rc;
   L.p.packed = 1;
+  if (b->dim % 64 == 0) {
+    for (int k = 0; k < 3; ++k) {
+      const int h = L.p.tile_n >> k;
+      if (h < TC_PACK) break;
+      for (int r = 0; r < 8; ++r) {
+        rc = make_tmap_ilv(&L.tm.pk[k][r], b->d_tokens, b->dtype, r, (b->n_d_tokens - r) / 8, b->dim, (uint32_t)h);
+        if (rc) return rc;
+      }
+    }
+    L.p.ilv = 1;
+  }
   L.p.d_tok_off = pk;
   L.p.src_row = src;
   L.p.doc_len = len;

@@ -86,6 +86,16 @@ __device__ __forceinline__ void tma_load_2d_hint(void* dst, const void* tmap, ui
       : "memory");
 }
 
+// 4-D tiled tensor load (coordinates c0..c3), L2 cache hint
+__device__ __forceinline__ void tma_load_4d_hint(void* dst, const void* tmap, uint64_t* bar, int32_t c0, int32_t c1,
+                                                 int32_t c2, int32_t c3, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4, "
+      "%5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
+      : "memory");
+}
+
 // 1-D bulk copy global -> shared (size and addresses multiples of 16), completion on an mbarrier
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -155,11 +165,12 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 // ----------------------------------------------------------------- descriptors
 // Shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 B,
 // 8-row core groups 1024 B apart (SBO), version 1 (sm_100), base offset 0.
-__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t smem_addr) {
+// `sbo` overrides the 8-row group stride (interleaved layouts keep several K blocks per group).
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t smem_addr, uint32_t sbo = 1024u) {
   uint64_t d = 0;
   d |= (uint64_t)((smem_addr & 0x3FFFFu) >> 4);      // start address
   d |= (uint64_t)(16u >> 4) << 16;                   // leading byte offset (unused for SW128 K-major)
-  d |= (uint64_t)(1024u >> 4) << 32;                 // stride byte offset
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;       // stride byte offset
   d |= (uint64_t)1 << 46;                            // descriptor version (sm_100)
   d |= (uint64_t)2 << 61;                            // layout: SWIZZLE_128B
   return d;

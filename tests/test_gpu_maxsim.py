@@ -215,6 +215,35 @@ def test_resident_corpus_rerank_matches_oracle():
             corpus.rerank_topk(qt, qo, np.full(int(co[-1]), 500), co, k, mode=mode)
 
 
+@pytest.mark.parametrize("dt,d,tail", [("f16", 128, 3), ("bf16", 256, 5), ("f16", 64, 7), ("f16", 512, 1),
+                                        ("bf16", 96, 6)])
+def test_packed_corpus_every_score_at_the_corpus_end(dt, d, tail):
+    """Every packed score (k = pool size) against the oracle when the corpus ends off an 8-row group:
+    the interleaved 4-D maps stop at their last whole group, boxes past it take the 8-row 2-D path."""
+    from paper_2602_02827_b200.batch import Corpus, to_torch_tokens
+
+    rng = np.random.default_rng(d + tail)
+    lens = np.concatenate([rng.integers(1, 300, size=60), [8 * 37 + tail, 40 + tail, tail]])
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    toks = W._cast(W._unit(rng.standard_normal((int(off[-1]), d))), dt)
+    corpus = Corpus(toks, off, dtype=storage_dtype(dt))
+    n = len(lens)
+    nd = 24
+    qs = [W._cast(W._unit(rng.standard_normal((int(rng.integers(1, 33)), d))), dt) for _ in range(3)]
+    # every pool holds the last three corpus documents, in shuffled positions
+    cands = [rng.permutation(np.concatenate([rng.choice(n - 3, nd - 3, replace=False), [n - 3, n - 2, n - 1]]))
+             for _ in range(3)]
+    qt = torch.cat([to_torch_tokens(q, storage_dtype(dt)) for q in qs]).pin_memory()
+    qo = np.concatenate([[0], np.cumsum([q.shape[0] for q in qs])]).astype(np.int64)
+    co = np.arange(4, dtype=np.int64) * nd
+    idx, val = corpus.rerank_topk(qt, qo, np.concatenate(cands), co, nd)
+    docs64 = [W.to_float64(toks[off[i]:off[i + 1]], dt) for i in range(n)]
+    for q in range(3):
+        s, _, _ = maxsim_ref.score_query(W.to_float64(qs[q], dt), [docs64[c] for c in cands[q]], nd)
+        assert sorted(idx[q].tolist()) == list(range(nd))
+        np.testing.assert_allclose(val[q].numpy(), s[idx[q].numpy()], rtol=1e-3, atol=1e-3)
+
+
 @pytest.mark.parametrize("dt,lq,d", [("f16", 32, 128), ("bf16", 48, 128), ("bf16", 64, 256), ("f16", 100, 96)])
 def test_packed_corpus_scores_match_oracle_on_config_shapes(dt, lq, d):
     """Packed streaming from the corpus: per-document 8-row alignment, docs across tiles, 1-token docs."""
