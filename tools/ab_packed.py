@@ -21,6 +21,9 @@ corpus = Corpus(b.d_tokens, do)
 rng = np.random.default_rng(0)
 nq = b.n_queries
 cand = np.concatenate([qd[q] + rng.permutation(int(qd[q + 1] - qd[q])) for q in range(nq)]).astype(np.int64)
+order = os.environ.get("ORDER", "random")  # "sorted": each query's candidates in corpus-row order (locality bound)
+if order == "sorted":
+    cand = np.concatenate([np.sort(cand[qd[q]:qd[q + 1]]) for q in range(nq)])
 cand_t = torch.from_numpy(cand).pin_memory()
 qh = b.q_tokens.cpu().pin_memory()
 k = 10
@@ -51,5 +54,5 @@ t0 = time.perf_counter()
 for _ in range(n):
     corpus.rerank_topk(qh, qo, cand_t, qd, k)
 e2e_ms = (time.perf_counter() - t0) * 1e3 / n
-print(json.dumps({"lib": os.environ.get("CBX_LIB", "default"), "cfg": cfg, "scores_bit_equal": equal,
+print(json.dumps({"lib": os.environ.get("CBX_LIB", "default"), "cfg": cfg, "order": order, "scores_bit_equal": equal,
                   "max_abs_diff": maxdiff, "device_ms": dev_ms, "e2e_ms": e2e_ms}))
