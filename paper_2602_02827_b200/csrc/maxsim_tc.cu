@@ -30,14 +30,22 @@
 
 namespace cbx {
 
-constexpr int TC_THREADS = 256;
-constexpr int TC_EPI_WARP0 = 4;
+#ifndef CBX_TC_EPI_WARP0
+#define CBX_TC_EPI_WARP0 4  // first of the four epilogue warps (warp % 4 = its TMEM lane quarter)
+#endif
+constexpr int TC_THREADS = (CBX_TC_EPI_WARP0 + 4) * 32;
+constexpr int TC_EPI_WARP0 = CBX_TC_EPI_WARP0;
+static_assert(TC_EPI_WARP0 % 4 == 0, "epilogue warps must cover TMEM lane quarters 0..3 in order");
 constexpr int TC_ACC_BUFS = 4;
 constexpr int TC_MAX_TILE_N = 128;
 constexpr int TC_MAX_STAGES = 8;
 #ifndef CBX_PACK_ALIGN
 #define CBX_PACK_ALIGN 32
 #endif
+#ifndef CBX_PK_PRODUCERS
+#define CBX_PK_PRODUCERS 3  // packed-mode TMA issuer warps: warp 0 plus warps 2.. (A/B knob for tools/mkvar.sh)
+#endif
+static_assert(CBX_PK_PRODUCERS >= 1 && CBX_PK_PRODUCERS <= CBX_TC_EPI_WARP0 - 1, "producers must end before the epilogue");
 constexpr int TC_PACK = CBX_PACK_ALIGN;  // packed-mode row granularity (power of two, >= 8)
 
 struct TcParams {
@@ -217,13 +225,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  if (warp == 0 || (p.packed && (warp == 2 || (warp == 3 && p.stages >= 3)))) {
+  if (warp == 0 || (p.packed && warp >= 2 && warp <= CBX_PK_PRODUCERS && warp - 1 < p.stages)) {
     // ------------------------------------------------------------ TMA producers (lane 0 issues)
     // Warp 0 loads the query and, in packed mode, shares the document tiles round-robin with warps 2
     // and 3 (packed tiles need several small boxes each; three issuers keep the ring full).
     // a producer may only run one ring lap ahead of the slowest one: np <= stages keeps every
     // empty-barrier parity wait unambiguous
-    const int np = p.packed ? (p.stages < 3 ? p.stages : 3) : 1;
+    const int np = p.packed ? (p.stages < CBX_PK_PRODUCERS ? p.stages : CBX_PK_PRODUCERS) : 1;
     const int pi = warp == 0 ? 0 : warp - 1;
     uint32_t qphase = 0, tg = 0;
     const uint64_t pol = ptx::policy_evict_first();
