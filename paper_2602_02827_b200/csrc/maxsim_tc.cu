@@ -696,9 +696,11 @@ struct TcLaunch {
   int grid;
 };
 
-static int prepare_tc(const cbx_batch* b, const void* d_rows, int64_t n_rows, float* scores, TcLaunch& L) {
+static int prepare_tc(const cbx_batch* b, const void* d_rows, int64_t n_rows, float* scores, TcLaunch& L,
+                      int tile_cap = 128) {
   const int kblocks = (b->dim + 63) / 64;
-  const int tile_n = kblocks <= 4 ? 128 : 32;  // d <= 256: N=128 MMAs; d=512: 32 rows (smem)
+  int tile_n = kblocks <= 4 ? 128 : 32;  // d <= 256: N=128 MMAs; d=512: 32 rows (smem)
+  if (tile_n > tile_cap) tile_n = tile_cap;
   const int nq = (b->max_lq + 31) / 32;
   const int rep = nq == 3 ? 1 : 4 / nq;
   const int lqp = nq * 32;
@@ -727,7 +729,7 @@ static int prepare_tc(const cbx_batch* b, const void* d_rows, int64_t n_rows, fl
   p.doc_len = nullptr;
   p.n_tokens_dev = nullptr;
   p.ilv = 0;
-  p.k8 = tile_n == 128 ? 4 : 2;  // d[k8] = 8-row boxes
+  p.k8 = tile_n == 128 ? 4 : tile_n == 64 ? 3 : 2;  // d[k8] = 8-row boxes
   p.corpus_rows = n_rows;
   p.n_queries = b->n_queries;
   p.n_docs = b->n_docs;
@@ -788,7 +790,10 @@ int launch_maxsim_tc_packed(const cbx_batch* b, const int64_t* corpus_off, int64
   plan_add_kernel<<<(unsigned)nb, PL_THREADS, 0, stream>>>(pk, n, btot, nb);
   CBX_LAUNCH_CHECK("plan_add_kernel launch");
   TcLaunch L;
-  int rc = prepare_tc(b, b->d_tokens, b->n_d_tokens, scores, L);
+#ifndef CBX_PK_TILE_N
+#define CBX_PK_TILE_N 128
+#endif
+  int rc = prepare_tc(b, b->d_tokens, b->n_d_tokens, scores, L, CBX_PK_TILE_N);
   if (rc) return rc;
   L.p.packed = 1;
   if (b->dim % 64 == 0) {
