@@ -7,22 +7,30 @@ One "step" = one pass of the hot path over one batch: the MaxSim score of
 every candidate of every query (tcgen05 dense scorer, P1) + per-query Top-K.
 The workload is BASELINE.json configs[1] ("cfg2": 256 queries x 1000
 candidates, Lq = 32, d = 128, fp16, lognormal doc lengths, K = 10), drawn on
-the device (synthetic, seeded by rank). Inputs (11.7 GB of doc tokens)
-exceed L2 (126 MB), so no flush is needed between steps.
+the device (synthetic; every query from its own seeded generator). Inputs
+(11.7 GB of doc tokens) exceed L2 (126 MB), so no flush is needed between
+steps.
+
+Multi-GPU (one process per GPU): under torchrun the ranks come from the
+environment; ``--gpus N`` without WORLD_SIZE spawns the N ranks itself
+(127.0.0.1 rendezvous, NCCL). The 256 queries are STRONG-scaled: rank r holds
+the contiguous query block workloads.query_blocks(...)[r], balanced by doc
+tokens, and no collective touches the data path (the queries are
+independent); value = all queries' cells / max-over-ranks time.
 
 The JSON line also carries the Col-Bandit loop (P2) on the same batch
 ("bandit": one CTA per query, default BanditConfig, seed (0, q)), with its
-revealed-cell throughput, gather bandwidth and CPU-oracle parity.
-
-"bandit_sharded" is the document-sharded Col-Bandit on cfg4 (one query, 100k
-candidates split over the ranks, one 8-byte all-reduce per iteration), with
-its single-GPU persistent-kernel time and trace equality beside it.
+revealed-cell throughput, gather bandwidth and CPU-oracle parity; cfg4's
+document-sharded exhaustive Top-K ("p1_sharded": per-rank scorer + local
+Top-100, one NCCL all-gather of 100 (score, id) pairs per rank, device merge);
+the Stage-1 scan + reranker facade ("stage1"); and cfg4's document-sharded
+Col-Bandit ("bandit_sharded").
 
 ``--impl reference`` times the reference's CPU algorithm (the oracle port in
 oracle/maxsim_ref: float64 GEMM + column max + math.fsum + lexsort) on the
 box's host cores, one process per core, for the same metric and config.
-Multi-GPU: one process per GPU, each with its own batch (weak scaling, no
-collective on the data path); value = all ranks' cells / max-over-ranks time.
+``--dry-run`` exercises the launcher, the query sharding and the max-over-ranks
+reduction without a GPU (gloo; the CPU test of the multi-rank path).
 """
 
 from __future__ import annotations
@@ -140,6 +148,32 @@ def _blas_one_thread():
         return None
 
 
+# ---------------------------------------------------------------------------- collectives
+def _dist():
+    import torch.distributed as dist
+
+    return dist if dist.is_available() and dist.is_initialized() else None
+
+
+def _reduce(values, op="max"):
+    """All-reduce a list of floats over the ranks (float64; NCCL or gloo); identity at world 1."""
+    import torch
+
+    dist = _dist()
+    if dist is None:
+        return [float(v) for v in values]
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.cpu().tolist()
+
+
+def _barrier():
+    dist = _dist()
+    if dist is not None:
+        dist.barrier()
+
+
 # ---------------------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local_rank):
     import numpy as np
@@ -149,8 +183,13 @@ def run_ours(args, rank, world, local_rank):
     from paper_2602_02827_b200.batch import HostBatch, maxsim_scores, rerank_topk_host, topk
 
     torch.cuda.set_device(local_rank)
-    cfg = W.CONFIGS[args.config]
-    batch, host_off = W.gen_batch_device(cfg, n_queries=args.queries, seed=rank)
+    cfg, lens_all, lqs_all = W.batch_plan(args.config, args.queries, seed=0)
+    nq_all = len(lqs_all)
+    if nq_all < world:
+        raise ValueError(f"{nq_all} queries cannot be sharded over {world} ranks")
+    blocks = W.query_blocks(lens_all, world)
+    qa, qb = blocks[rank]
+    batch, host_off = W.gen_batch_device(cfg, n_queries=args.queries, seed=0, queries=(qa, qb))
     torch.cuda.synchronize()
     nq, K = batch.n_queries, cfg.k
     elem = batch.d_tokens.element_size()
@@ -158,7 +197,7 @@ def run_ours(args, rank, world, local_rank):
     lq = np.diff(qo)
     ndocs = np.diff(qd)
     qtok = do[qd[1:]] - do[qd[:-1]]
-    cells_per_step = int((ndocs * lq).sum())
+    cells_total = int(lens_all.shape[1] * lqs_all.sum())  # every query of the job, all ranks
     alg_bytes = int(batch.d_tokens.numel() * elem + batch.q_tokens.numel() * elem + 4 * batch.n_docs)
     alg_flops = int(2 * (qtok * lq).sum() * batch.dim)
     hbm_peak, tf_peak, peak_kind = _peaks()
@@ -180,8 +219,7 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    _barrier()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clocks:
@@ -191,12 +229,8 @@ def run_ours(args, rank, world, local_rank):
             idx, val = step(evs[i])
         stop.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    t = torch.tensor([start.elapsed_time(stop)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms_step = float(t.item()) / args.steps
+    _barrier()
+    ms_step = _reduce([start.elapsed_time(stop)])[0] / args.steps
     kern_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     topk_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
 
@@ -205,22 +239,23 @@ def run_ours(args, rank, world, local_rank):
         achieved = alg_bytes / (kern_ms / 1e3) / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tpath):
+        if os.path.exists(tpath) and world == 1:
             traffic = json.load(open(tpath)).get(args.config)
         result = {
-            "metric": METRIC, "value": cells_per_step * world / (ms_step / 1e3), "unit": UNIT, "n_gpus": world,
+            "metric": METRIC, "value": cells_total / (ms_step / 1e3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
-            "data": "synthetic (device RNG, BASELINE.json configs[1] recipe)",
-            "config": {"workload": f"{cfg.name}: {nq} queries x {cfg.n_docs} docs, Lq={cfg.lq[0]}, d={cfg.dim}, "
+            "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
+            "data": "synthetic (device RNG per query, BASELINE.json configs[1] recipe)",
+            "config": {"workload": f"{cfg.name}: {nq_all} queries x {cfg.n_docs} docs, Lq={cfg.lq[0]}, d={cfg.dim}, "
                                    f"lognormal lengths (mean 180, sigma 0.5, clip [16,512]), {cfg.dtype}, K={K}",
-                       "queries_per_gpu": nq, "doc_tokens_per_gpu": int(batch.d_tokens.shape[0]),
-                       "l2": "inputs (%.1f GB) exceed L2 (126 MB); no flush" % (alg_bytes / 1e9),
-                       "parallelism": f"query-sharded x{world} (no collective)"},
-            "queries_per_s": nq * world / (ms_step / 1e3),
+                       "queries": nq_all, "query_blocks": blocks,
+                       "doc_tokens": int(lens_all.sum()), "doc_tokens_rank0": int(batch.d_tokens.shape[0]),
+                       "l2": "inputs (%.1f GB per rank) exceed L2 (126 MB); no flush" % (alg_bytes / 1e9),
+                       "parallelism": f"query-sharded x{world}, blocks balanced by doc tokens (no collective)"},
+            "queries_per_s": nq_all / (ms_step / 1e3),
             "scorer_ms": kern_ms, "topk_ms": topk_ms,
-            "roofline": {"bound": "hbm", "kernel": "maxsim_tc_kernel", "achieved": achieved, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved / hbm_peak, "peak_kind": peak_kind,
+            "roofline": {"bound": "hbm", "kernel": "maxsim_tc_kernel (rank 0)", "achieved": achieved,
+                         "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "peak_kind": peak_kind,
                          "alg_bytes_per_launch": alg_bytes, "traffic": traffic,
                          "tensor_tflops": alg_flops / (kern_ms / 1e3) / 1e12, "tensor_peak": tf_peak},
             "clocks": clocks.summary(),
@@ -254,11 +289,12 @@ def run_ours(args, rank, world, local_rank):
                                       "sample": f"{n_chk} {cfg.name} queries through oracle/maxsim_ref (float64 GEMM "
                                                 f"+ column max + math.fsum + lexsort, BLAS 1 thread), {cpu_s:.1f} s"}
         del lim
+    _barrier()
 
     # ------------------------------------------------ end-to-end through the public host API
     # The reranking service keeps the corpus resident in HBM (Corpus = ColBanditReranker.fit); every
     # step ships the queries and their candidate id lists host -> device (each query's candidates in a
-    # shuffled order), gathers the candidates, scores, selects Top-K and reads it back (pinned host).
+    # shuffled order), streams the candidates out of the corpus, scores, selects Top-K and reads it back.
     if not args.no_e2e:
         from paper_2602_02827_b200.batch import Corpus
 
@@ -270,8 +306,7 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(2):
             corpus.rerank_topk(q_host, qo, cand_t, qd, K)
         torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
+        _barrier()
         e_steps = max(3, args.steps)
         t0 = time.perf_counter()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -281,22 +316,19 @@ def run_ours(args, rank, world, local_rank):
         e1.record(stream)
         torch.cuda.synchronize()
         wall_ms = (time.perf_counter() - t0) * 1e3 / e_steps
-        t = torch.tensor([max(e0.elapsed_time(e1) / e_steps, wall_ms)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e_ms, = _reduce([max(e0.elapsed_time(e1) / e_steps, wall_ms)])
+        h2d, = _reduce([q_host.numel() * q_host.element_size() + cand.nbytes + 2 * 8 * (nq + 1)], "sum")
         if rank == 0:
-            e_ms = float(t.item())
             got_docs = np.take_along_axis(cand.reshape(nq, -1), oi.numpy().astype(np.int64), axis=1) \
                 if np.all(np.diff(qd) == qd[1] - qd[0]) else None
             ref_docs = idx.cpu().numpy().astype(np.int64) + qd[:-1, None]
-            result["e2e"] = {"value": cells_per_step * world / (e_ms / 1e3), "unit": UNIT,
-                             "h2d_bytes_per_step": int(q_host.numel() * q_host.element_size() + cand.nbytes
-                                                       + 2 * 8 * (nq + 1)),
-                             "d2h_bytes_per_step": int(nq * K * 8), "ms_per_step": e_ms,
+            result["e2e"] = {"value": cells_total / (e_ms / 1e3), "unit": UNIT,
+                             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(nq_all * K * 8),
+                             "ms_per_step": e_ms,
                              "api": "batch.Corpus.rerank_topk: corpus resident in HBM (fit once, untimed); per step "
                                     "H2D query tokens + candidate ids, TMA streams candidates straight from the "
                                     "corpus (32-row packed layout), score, Top-K, D2H Top-K; "
-                                    "max of device-event and host wall time",
+                                    "max of device-event and host wall time, max over ranks",
                              "topk_equals_device_path": bool(got_docs is not None and
                                                              np.array_equal(got_docs, ref_docs))}
         del corpus
@@ -305,24 +337,24 @@ def run_ours(args, rank, world, local_rank):
         out = (torch.empty((nq, K), dtype=torch.int32).pin_memory(), torch.empty((nq, K)).pin_memory())
         rerank_topk_host(hb, K, out=out)
         torch.cuda.synchronize()
+        _barrier()
         e0.record(stream)
         for _ in range(2):
             rerank_topk_host(hb, K, out=out)
         e1.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / 2], dtype=torch.float64, device="cuda")
-        if world > 1:
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        cold_ms, = _reduce([e0.elapsed_time(e1) / 2])
+        cold_h2d, = _reduce([hb.h2d_bytes], "sum")
         if rank == 0:
-            result["e2e_cold"] = {"value": cells_per_step * world / (float(t.item()) / 1e3), "unit": UNIT,
-                                  "h2d_bytes_per_step": hb.h2d_bytes, "d2h_bytes_per_step": int(nq * K * 8),
-                                  "ms_per_step": float(t.item()),
-                                  "api": "batch.rerank_topk_host: all 11.7 GB of doc tokens H2D every step (PCIe bound)"}
+            result["e2e_cold"] = {"value": cells_total / (cold_ms / 1e3), "unit": UNIT,
+                                  "h2d_bytes_per_step": int(cold_h2d), "d2h_bytes_per_step": int(nq_all * K * 8),
+                                  "ms_per_step": cold_ms,
+                                  "api": "batch.rerank_topk_host: all doc tokens H2D every step (PCIe bound)"}
         del hb
 
-    # ------------------------------------------------ P2: the Col-Bandit loop on the same batch
-    # the sections below are reported beside the headline; a failure in one is recorded, not fatal
-    # (every rank runs the same code on the same shapes, so a failure is symmetric across ranks)
+    # ------------------------------------------------ the sections below are reported beside the headline;
+    # a failure in one is recorded, not fatal (every rank runs the same code on the same shapes, so a
+    # failure is symmetric across ranks)
     def section(name, fn):
         try:
             out = fn()
@@ -333,18 +365,96 @@ def run_ours(args, rank, world, local_rank):
             result[name] = out
 
     if not args.no_bandit:
-        section("bandit", lambda: run_bandit(args, batch, host_off, cfg, rank, world))
-    # ------------------------------------------------ Stage 1 (candidate scan) + the reranker facade, cfg4 corpus
+        section("bandit", lambda: run_bandit(args, batch, host_off, cfg, rank, world, qa))
     del batch
     torch.cuda.empty_cache()
+    if not args.no_p1_sharded:
+        section("p1_sharded", lambda: run_p1_sharded(args, rank, world))
+        torch.cuda.empty_cache()
     if not args.no_stage1:
         section("stage1", lambda: run_stage1(args, rank, world))
-    # ------------------------------------------------ P2 document-sharded over the ranks (cfg4)
     if not args.no_p2_sharded:
         torch.cuda.empty_cache()
         section("bandit_sharded", lambda: run_p2_sharded(args, rank, world))
     if rank == 0:
         print(json.dumps(result), flush=True)
+
+
+def run_p1_sharded(args, rank, world):
+    """cfg4 (one query, 100k candidates) exhaustive Top-100, documents sharded over the ranks:
+    rank r scores its token-balanced contiguous document range with the tcgen05 scorer, takes its local
+    Top-100 on the device, and ONE all-gather of 100 (score, global id) pairs per rank (NCCL over NVLink)
+    feeds a device Top-K merge over the gathered lists, which ranks by (-score, id) exactly like the 1-GPU
+    Top-K (rank-major gather order = id order for equal scores). Rank 0 checks the merged list against the
+    single-GPU Top-100 of the whole pool."""
+    import numpy as np
+    import torch
+
+    from paper_2602_02827_b200 import workloads as W
+    from paper_2602_02827_b200.batch import TokenBatch, maxsim_scores, topk
+    from paper_2602_02827_b200.dist import balanced_ranges
+
+    cfg = W.CONFIGS["cfg4"]
+    K = cfg.k
+    b, (qo, do, qd) = W.gen_batch_device(cfg, n_queries=1, seed=0)  # the same pool on every rank
+    N = b.n_docs
+    single = None
+    if rank == 0:
+        s_all = maxsim_scores(b)
+        single = topk(s_all, b.q_doc_off, K, N)[0].cpu().numpy().ravel().tolist()
+        del s_all
+    lo, hi = balanced_ranges(do, world)[rank]
+    local = (do[lo:hi + 1] - do[lo]).astype(np.int64)
+    shard = b.d_tokens[int(do[lo]):int(do[hi])].clone()
+    sb = TokenBatch.from_device(b.q_tokens, b.q_tok_off, shard, torch.from_numpy(local).cuda(),
+                                torch.tensor([0, hi - lo], dtype=torch.int64, device="cuda"), False,
+                                host_offsets=(qo, local, np.array([0, hi - lo], np.int64)))
+    del b
+    torch.cuda.empty_cache()
+    dist = _dist()
+    kk = min(K, hi - lo)
+    scores = torch.empty(hi - lo, dtype=torch.float32, device="cuda")
+    g_s = torch.empty(world * K, dtype=torch.float32, device="cuda")
+    g_i = torch.empty(world * K, dtype=torch.int64, device="cuda")
+    off_m = torch.tensor([0, world * K], dtype=torch.int64, device="cuda")
+
+    def step():
+        maxsim_scores(sb, out=scores)
+        li, lv = topk(scores, sb.q_doc_off, kk, hi - lo)
+        s = torch.full((K,), float("-inf"), dtype=torch.float32, device="cuda")
+        i = torch.full((K,), -1, dtype=torch.int64, device="cuda")
+        s[:kk] = lv.view(-1)
+        i[:kk] = li.view(-1).to(torch.int64) + lo
+        if dist is not None:
+            dist.all_gather_into_tensor(g_s, s)
+            dist.all_gather_into_tensor(g_i, i)
+        else:
+            g_s.copy_(s)
+            g_i.copy_(i)
+        mi, mv = topk(g_s, off_m, K, world * K)
+        return g_i[mi.view(-1).to(torch.int64)]
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    _barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        ids = step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms, = _reduce([e0.elapsed_time(e1) / args.steps])
+    merged = ids.cpu().numpy().tolist()
+    if rank != 0:
+        return None
+    T = int(qo[1] - qo[0])
+    return {"what": "cfg4 exhaustive Top-100 (one query, 100k docs, Lq=32, d=128, f16) document-sharded over "
+                    f"{world} rank(s): per-rank tcgen05 scorer + local Top-100, one all-gather of 100 (score, id) "
+                    "pairs per rank, device Top-K merge by (-score, id)",
+            "ranks": world, "ms": ms, "cells_per_s": N * T / (ms / 1e3),
+            "doc_tokens_rank0": int(local[-1]), "exchange_bytes_per_rank": K * 12,
+            "topk_equal_single_gpu": merged == single, "gpu_launches": 3 + (2 if world > 1 else 0)}
 
 
 def run_p2_sharded(args, rank, world):
@@ -515,7 +625,9 @@ def _bandit_traffic(name):
     return json.load(open(tpath)).get(f"bandit_{name}") if os.path.exists(tpath) else None
 
 
-def run_bandit(args, batch, host_off, cfg, rank, world):
+def run_bandit(args, batch, host_off, cfg, rank, world, qa=0):
+    """The Col-Bandit loop on this rank's query block (one CTA per run), timed on the device; the job's
+    totals (runs, reveals, gathered bytes) are summed over the ranks and the time is the max over ranks."""
     import numpy as np
     import torch
 
@@ -524,7 +636,8 @@ def run_bandit(args, batch, host_off, cfg, rank, world):
 
     qo, do, qd = host_off
     nq = batch.n_queries
-    jobs = [BanditJob(BanditConfig(k=cfg.k, seed=(0, q)), int(qd[q + 1] - qd[q]), int(qo[q + 1] - qo[q]), q,
+    # seeds follow the reference's (random_state, query_index) convention with the GLOBAL query index
+    jobs = [BanditJob(BanditConfig(k=cfg.k, seed=(0, qa + q)), int(qd[q + 1] - qd[q]), int(qo[q + 1] - qo[q]), q,
                       int(qd[q]), (-1.0, 1.0)) for q in range(nq)]
     lens = np.diff(do)
     elem = batch.d_tokens.element_size()
@@ -533,50 +646,53 @@ def run_bandit(args, batch, host_off, cfg, rank, world):
     for _ in range(max(1, min(args.warmup, 2))):
         collect(launch_batch(prep), jobs, list(prep["results"]), return_traces=False)
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    _barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     raw = launch_batch(prep)
     e1.record()
     torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms = float(t.item())
+    ms, = _reduce([e0.elapsed_time(e1)])
     res = collect(raw, jobs, list(prep["results"]))
     # end to end through the public call (host seeding + descriptors + launches + traces back)
+    _barrier()
     t0 = time.perf_counter()
     res_e2e = run_batch(jobs, batch=batch)
-    e2e_ms = (time.perf_counter() - t0) * 1e3
-    assert [r.reveals for r in res_e2e] == [r.reveals for r in res]
-    if rank != 0:
-        return None
+    e2e_ms, = _reduce([(time.perf_counter() - t0) * 1e3])
+    assert all(a.reveals == b.reveals for a, b in zip(res_e2e, res))
     reveals = sum(len(r.reveals) for r in res)
     gather = 0
     for j, r in zip(jobs, res):
-        if r.reveals:
-            gather += int(lens[np.array([i for i, _, _ in r.reveals]) + j.row_begin].sum()) * batch.dim * elem
-    hbm_peak, _, peak_kind = _peaks()
+        if len(r.reveals):
+            gather += int(lens[r.reveals.i.astype(np.int64) + j.row_begin].sum()) * batch.dim * elem
     cov = np.array([r.coverage for r in res])
+    runs_all, reveals_all, gather_all, iters_all, cov_sum = _reduce(
+        [len(jobs), reveals, gather, sum(r.iterations for r in res), cov.sum()], "sum")
+    cov_min, = _reduce([-cov.min()])
+    cov_max, = _reduce([cov.max()])
+    if rank != 0:
+        return None
+    hbm_peak, _, peak_kind = _peaks()
     out = {"what": "Col-Bandit run() per query (one CTA each), BanditConfig defaults, generic bounds (-1, 1), "
-                   "seed (0, q)",
-           "runs": len(jobs), "ms": ms, "queries_per_s": len(jobs) * world / (ms / 1e3),
-           "revealed_cells_per_s": reveals * world / (ms / 1e3),
-           "iterations": int(sum(r.iterations for r in res)),
-           "coverage_mean": float(cov.mean()), "coverage_min": float(cov.min()), "coverage_max": float(cov.max()),
-           "roofline": {"bound": "hbm (gather)", "achieved": gather / (ms / 1e3) / 1e9, "peak": hbm_peak,
-                        "unit": "GB/s", "frac": gather / (ms / 1e3) / 1e9 / hbm_peak, "peak_kind": peak_kind,
-                        "alg_bytes": gather,
+                   "seed (0, q); queries sharded over the ranks like the headline",
+           "runs": int(runs_all), "ms": ms, "queries_per_s": runs_all / (ms / 1e3),
+           "revealed_cells_per_s": reveals_all / (ms / 1e3),
+           "iterations": int(iters_all),
+           "coverage_mean": cov_sum / runs_all, "coverage_min": -cov_min, "coverage_max": cov_max,
+           "roofline": {"bound": "hbm (gather)", "achieved": gather_all / (ms / 1e3) / 1e9 / world,
+                        "peak": hbm_peak, "unit": "GB/s per GPU",
+                        "frac": gather_all / (ms / 1e3) / 1e9 / world / hbm_peak, "peak_kind": peak_kind,
+                        "alg_bytes": int(gather_all),
                         "note": "algorithmic gather = sum over reveals of L_i*d*s (warm-up included); repeated "
                                 "boundary rows hit L2/L1, so this can exceed DRAM traffic",
-                        "traffic": _bandit_traffic(cfg.name),
+                        "traffic": _bandit_traffic(cfg.name) if world == 1 else None,
                         "traffic_note": "dram__bytes_read+write of one bandit_kernel launch on this config from "
-                                        "the committed ncu capture (profiles/r1_ncu_bandit_cfg2_details.txt; "
-                                        "L2 hit rate 24 %)"},
+                                        "the committed ncu capture (profiles/)"},
            "gpu_launches": 1 + (2 if prep["n_prewarm"] else 0),
-           "e2e": {"ms": e2e_ms, "revealed_cells_per_s": reveals * world / (e2e_ms / 1e3),
-                   "api": "bandit.run_batch(jobs, batch): host seeding + descriptors + launch + traces D2H"}}
+           "e2e": {"ms": e2e_ms, "revealed_cells_per_s": reveals_all / (e2e_ms / 1e3),
+                   "ratio_to_device": e2e_ms / ms,
+                   "api": "bandit.run_batch(jobs, batch): host seeding + descriptors + launch + compacted trace "
+                          "D2H (RunResult.reveals as numpy-backed Reveals)"}}
     # parity + CPU baseline on sampled queries: the oracle loop must reproduce the device trace
     from oracle import bandit_ref, maxsim_ref
 
@@ -586,10 +702,10 @@ def run_bandit(args, batch, host_off, cfg, rank, world):
         qt, docs = _query_host(batch, host_off, q)
         t0 = time.perf_counter()
         cells = maxsim_ref.cell_matrix(qt, docs)
-        ref = bandit_ref.run(cells, -1.0, 1.0, cfg.k, seed=(0, q))
+        ref = bandit_ref.run(cells, -1.0, 1.0, cfg.k, seed=(0, qa + q))
         cpu_s += time.perf_counter() - t0
         cpu_rev += len(ref.reveals)
-        same &= (ref.reveals == res[q].reveals and ref.topk == res[q].topk)
+        same &= (res[q].reveals == ref.reveals and ref.topk == res[q].topk)
         cov_err = max(cov_err, abs(ref.coverage - res[q].coverage))
         n_chk += 1
         if n_chk >= args.check_queries and cpu_s >= args.cpu_seconds / 2:
@@ -662,6 +778,78 @@ def run_reference(args):
     }), flush=True)
 
 
+def run_dry(args, rank, world):
+    """--dry-run: the multi-rank plumbing without a GPU (gloo): the query plan, this rank's block, a
+    host-side stand-in step timed per rank, the max-over-ranks time and the JSON line of rank 0."""
+    import numpy as np
+
+    from paper_2602_02827_b200 import workloads as W
+
+    cfg, lens_all, lqs_all = W.batch_plan(args.config, args.queries, seed=0)
+    blocks = W.query_blocks(lens_all, world)
+    qa, qb = blocks[rank]
+    _barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        tok = int(lens_all[qa:qb].sum())  # stand-in for scoring the block: its doc-token count
+    ms, = _reduce([(time.perf_counter() - t0) * 1e3 / args.steps])
+    tok_all, nq_all = _reduce([tok, qb - qa], "sum")
+    if rank == 0:
+        cells = int(lens_all.shape[1] * lqs_all.sum())
+        print(json.dumps({"metric": METRIC, "value": cells / max(ms, 1e-9) * 1e3, "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                          "scaling": "strong", "dry_run": True, "dtype": cfg.dtype,
+                          "config": {"workload": cfg.name, "queries": int(nq_all), "query_blocks": blocks,
+                                     "doc_tokens": int(tok_all)}}), flush=True)
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _spawned(local_rank, args, world, port):
+    """Entry of a rank spawned by ``bench.py --gpus N`` (no torchrun): the torchrun environment by hand."""
+    os.environ.update({"RANK": str(local_rank), "LOCAL_RANK": str(local_rank), "WORLD_SIZE": str(world),
+                       "LOCAL_WORLD_SIZE": str(world), "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    _rank_main(args)
+
+
+def _rank_main(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        # the reference's CPU algorithm runs once, on rank 0; other ranks exit without work
+        if rank == 0:
+            run_reference(args)
+        return
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        if args.dry_run:
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        if args.dry_run:
+            run_dry(args, rank, world)
+        else:
+            run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -676,30 +864,22 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-bandit", action="store_true")
+    ap.add_argument("--no-p1-sharded", action="store_true")
     ap.add_argument("--no-stage1", action="store_true")
     ap.add_argument("--no-p2-sharded", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="launcher/sharding/reduction only, no GPU (gloo)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        # no torchrun: spawn one process per GPU here (torchrun's environment, 127.0.0.1 rendezvous)
+        import torch.multiprocessing as tmp
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        if rank == 0:
-            run_reference(args)
+        tmp.start_processes(_spawned, args=(args, args.gpus, _free_port()), nprocs=args.gpus, join=True,
+                            start_method="spawn")
         return
-    if world > 1:
-        import torch
-
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl")
-    try:
-        run_ours(args, rank, world, local_rank)
-    finally:
-        if world > 1:
-            import torch
-
-            torch.distributed.destroy_process_group()
+    _rank_main(args)
 
 
 if __name__ == "__main__":

@@ -207,11 +207,13 @@ typedef struct cbx_pcg64 {
  * after that draw; every other draw happens on the device. */
 #define CBX_BANDIT_TREE 1
 #define CBX_BANDIT_PREWARMED 2
+#define CBX_BANDIT_MAX_COLS 128
+#define CBX_BANDIT_EDESC 3
 typedef struct cbx_bandit_run_desc {
   int64_t query;          /* token source: query index in the batch           */
   int64_t row_begin;      /* global doc index (token source) or matrix row of row 0 */
   int32_t n_rows;         /* pool size N                                      */
-  int32_t n_cols;         /* T (query tokens), 1..64                          */
+  int32_t n_cols;         /* T (query tokens), 1..128                         */
   int32_t k;              /* Top-K target, 1..N (k == 0 is answered on the host) */
   int32_t explore_mode;   /* CBX_EPSILON_GREEDY / CBX_STATIC_WARMUP / CBX_UNIFORM_ROW */
   int32_t n_warm;         /* static warm-up cell count                        */
@@ -236,7 +238,10 @@ typedef struct cbx_bandit_out {
   int32_t iterations;
   int32_t terminated_by;  /* CBX_TERM_* */
   int32_t status;         /* 0 ok; 1 both boundary rows exhausted (RuntimeError in the
-                             reference, bandit.py:311-312); 2 exact-sum capacity exceeded */
+                             reference, bandit.py:311-312); 2 exact-sum capacity exceeded;
+                             3 (CBX_BANDIT_EDESC) the descriptor breaks the shape contract
+                             (n_rows < 1, n_cols outside 1..128, k outside 1..min(n_rows, max_k)):
+                             nothing ran (ValueError) */
   int32_t pad;
 } cbx_bandit_out;
 
@@ -298,6 +303,16 @@ CBX_API int cbx_bandit_shard_step(const cbx_batch* b, const double* matrix, int6
                                   void* state, size_t state_bytes, void* step_state, int64_t* xchg,
                                   int32_t* topk, int32_t max_k, int32_t* trace_i, int32_t* trace_t,
                                   double* trace_v, cbx_bandit_out* out, void* stream);
+
+/* The loop's numpy Generator(PCG64) replica, exposed to pin it against numpy
+ * streams (tests/golden/pcg64_streams.json): starting from *state (host
+ * struct), draw j is Generator.random() (float64 bits in out[j]) when
+ * ops[j] == 0, else Generator.integers(ops[j]) (Lemire with rejection on
+ * buffered 32-bit halves; no draw for 1). ops/out/state_out are device
+ * pointers; state_out (may be NULL) receives the generator after the draws.
+ * Same code as the bandit loop's draws (bandit.py:133-134, 164, 314-315). */
+CBX_API int cbx_pcg64_draws(const cbx_pcg64* state, const uint32_t* ops, int64_t n_ops, uint64_t* out,
+                            cbx_pcg64* state_out, void* stream);
 
 /* Profiling hook: when set (device pointer to n_runs * 16 uint64), every
  * following cbx_bandit_run writes per-run SM-cycle counters of its phases

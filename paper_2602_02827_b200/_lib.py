@@ -12,8 +12,13 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("CBX_LIB") or os.path.join(_HERE, "libcbx.so")  # CBX_LIB: experimental builds
+LIB_PATH = os.path.join(_HERE, "libcbx.so")
+# A/B tooling only (tools/p2var.sh, tools/ab_packed.py): CBX_LIB names an experimental build, and it is honoured
+# only together with CBX_TOOLS=1 so that no test, smoke() or bench run can load anything but the in-tree library.
+if os.environ.get("CBX_TOOLS") == "1" and os.environ.get("CBX_LIB"):
+    LIB_PATH = os.environ["CBX_LIB"]
 
+CBX_ABI_VERSION = 1
 CBX_OK, CBX_EINVAL, CBX_ERANGE, CBX_ECUDA, CBX_EINTERNAL = 0, 1, 2, 3, 4
 CBX_F32, CBX_F16, CBX_BF16, CBX_F64 = 0, 1, 2, 3
 CBX_PATH_AUTO, CBX_PATH_TC, CBX_PATH_SIMT = 0, 1, 2
@@ -22,6 +27,8 @@ CBX_TERM_SEPARATION, CBX_TERM_EXHAUSTION = 0, 1
 CBX_BANDIT_ROW_SLACK = 64
 CBX_BANDIT_TREE = 1
 CBX_BANDIT_PREWARMED = 2
+CBX_BANDIT_MAX_COLS = 128
+CBX_BANDIT_EDESC = 3
 CBX_BANDIT_STEP_BYTES = 256
 CBX_SHARD_REVEAL, CBX_SHARD_WARMUP, CBX_SHARD_DONE = 0, 1, 2
 
@@ -115,6 +122,7 @@ SIGNATURES = {
     "cbx_token_norm_max": (_I, [_P, _I64, _I, _I, _P, _P]),
     "cbx_bandit_state_bytes": (_SZ, [_I64]),
     "cbx_bandit_set_profile": (None, [_P]),
+    "cbx_pcg64_draws": (_I, [_P, _P, _I64, _P, _P, _P]),
     "cbx_bandit_run": (_I, [_P, _P, _I64, _P, _I64, _I32, _P, _P, _P, _P, _SZ, _P, _I32, _P, _P, _P, _P, _P]),
     "cbx_bandit_prewarm": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P]),
     "cbx_bandit_shard_step": (_I, [_P, _P, _I64, _P, _I64, _I64, _I, _P, _P, _P, _P, _SZ, _P, _P, _P, _I32, _P, _P,

@@ -26,14 +26,14 @@ import numpy as np
 from . import _lib
 from .bounds import CellBounds, RadiusConfig
 
-__all__ = ["BanditConfig", "RunResult", "EXPLORE_MODES", "run", "run_batch", "prepare_batch", "launch_batch",
+__all__ = ["BanditConfig", "RunResult", "Reveals", "EXPLORE_MODES", "run", "run_batch", "prepare_batch", "launch_batch",
            "ceil_cells", "select_ambiguous",
            "select_token", "static_warmup", "init_one_per_row", "BanditJob"]
 
 EXPLORE_MODES = ("epsilon-greedy", "static-warmup", "uniform-row")
 _MODE_CODE = {"epsilon-greedy": _lib.CBX_EPSILON_GREEDY, "static-warmup": _lib.CBX_STATIC_WARMUP,
               "uniform-row": _lib.CBX_UNIFORM_ROW}
-MAX_COLS = 64
+MAX_COLS = 128  # CBX_BANDIT_MAX_COLS: two 64-bit unrevealed-column words per row
 TREE_ROWS = 0  # pools larger than this select boundary rows through tournament trees (measured faster at every size)
 
 
@@ -67,13 +67,72 @@ class BanditConfig:
         return RadiusConfig(self.alpha_ef, self.delta, self.c, self.union_mode)
 
 
+class Reveals(Sequence):
+    """The reveal trace of a run as three numpy columns (row i int32, column t int32, value float64).
+
+    Behaves like the reference's ``list[tuple[int, int, float]]`` (bandit.py:79-95): indexing yields
+    ``(int, int, float)`` tuples, slicing yields a list, and it compares equal to a list of tuples with the
+    same entries; the Python tuples are only built when they are asked for, so fetching a large batch of
+    runs costs one compact device-to-host copy instead of a tuple per revealed cell.
+    """
+
+    __slots__ = ("i", "t", "v", "_list")
+
+    def __init__(self, i, t, v):
+        self.i = np.asarray(i, dtype=np.int32)
+        self.t = np.asarray(t, dtype=np.int32)
+        self.v = np.asarray(v, dtype=np.float64)
+        self._list = None
+
+    @classmethod
+    def from_list(cls, reveals) -> "Reveals":
+        if isinstance(reveals, Reveals):
+            return reveals
+        n = len(reveals)
+        a = np.array([(i, t) for i, t, _ in reveals], dtype=np.int32).reshape(n, 2)
+        return cls(a[:, 0], a[:, 1], np.array([v for *_, v in reveals], dtype=np.float64))
+
+    def tolist(self) -> list:
+        if self._list is None:
+            self._list = list(zip(self.i.tolist(), self.t.tolist(), self.v.tolist()))
+        return self._list
+
+    def __len__(self) -> int:
+        return len(self.i)
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return self.tolist()[k]
+        return (int(self.i[k]), int(self.t[k]), float(self.v[k]))
+
+    def __iter__(self):
+        return iter(self.tolist())
+
+    def __eq__(self, other):
+        if isinstance(other, Reveals):
+            return (len(self) == len(other) and np.array_equal(self.i, other.i) and np.array_equal(self.t, other.t)
+                    and np.array_equal(self.v, other.v))
+        if isinstance(other, (list, tuple)):
+            return len(other) == len(self) and self.tolist() == [tuple(x) for x in other]
+        return NotImplemented
+
+    def __ne__(self, other):
+        eq = self.__eq__(other)
+        return eq if eq is NotImplemented else not eq
+
+    __hash__ = None
+
+    def __repr__(self) -> str:
+        return repr(self.tolist()) if len(self) <= 8 else f"Reveals({len(self)} cells: {self[:3]!r} ...)"
+
+
 @dataclass(frozen=True)
 class RunResult:
-    """bandit.py:79-95."""
+    """bandit.py:79-95 (``reveals`` is a :class:`Reveals`, which compares equal to the reference's list)."""
 
     topk: list[int]
     coverage: float
-    reveals: list[tuple[int, int, float]]
+    reveals: Sequence[tuple[int, int, float]]
     iterations: int
     terminated_by: str
 
@@ -142,21 +201,59 @@ class BanditJob:
     selection: str = "auto"  # "scan" | "tree" | "auto" (= tree for pools above TREE_ROWS)
 
 
+_PCG_MULT = 0x2360ED051FC65DA44385DF649FCCF645
+_M128 = (1 << 128) - 1
+_M64 = (1 << 64) - 1
+_SEED_CACHE: dict = {}
+
+
+def pcg64_seed_state(seed) -> tuple[int, int]:
+    """(state, inc) of ``np.random.Generator(PCG64(seed))`` right after seeding, without building a Generator.
+
+    numpy's PCG64 takes four 64-bit words from ``SeedSequence(seed).generate_state(4, uint64)``: initstate =
+    w0:w1, initseq = w2:w3, then pcg_setseq_128_srandom_r — state = 0, inc = initseq << 1 | 1, step, state +=
+    initstate, step (step: state = state * MULT + inc mod 2^128). ~4x cheaper than default_rng(seed), and
+    cached per seed (a sweep reuses each query's seed for every alpha). Checked against numpy in the tests.
+    """
+    key = seed if not isinstance(seed, list) else tuple(seed)
+    try:
+        return _SEED_CACHE[key]
+    except (KeyError, TypeError):
+        pass
+    w = [int(x) for x in np.random.SeedSequence(seed).generate_state(4, np.uint64)]
+    initstate, initseq = (w[0] << 64) | w[1], (w[2] << 64) | w[3]
+    inc = ((initseq << 1) | 1) & _M128
+    state = inc  # 0 * MULT + inc
+    state = (state + initstate) & _M128
+    state = (state * _PCG_MULT + inc) & _M128
+    try:
+        if len(_SEED_CACHE) > 65536:
+            _SEED_CACHE.clear()
+        _SEED_CACHE[key] = (state, inc)
+    except TypeError:
+        pass
+    return state, inc
+
+
 def _rng_state(seed, explore_mode, gamma_init, total_cells):
     """numpy seeding (+ the static warm-up draw) on the host; returns (pcg64 struct, warm cells)."""
-    g = np.random.default_rng(seed)
     warm = np.zeros(0, dtype=np.int32)
-    if explore_mode == "static-warmup":
-        m = ceil_cells(gamma_init, total_cells)
+    p = _lib.CbxPcg64()
+    m = ceil_cells(gamma_init, total_cells) if explore_mode == "static-warmup" else 0
+    if m == 0 and seed is not None:
+        s, inc = pcg64_seed_state(seed)
+        has32, buf = 0, 0
+    else:
+        g = np.random.default_rng(seed)
         if m:
             warm = np.asarray(g.choice(total_cells, size=m, replace=False), dtype=np.int32)
-    st = g.bit_generator.state
-    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
-    p = _lib.CbxPcg64()
-    p.state_hi, p.state_lo = s >> 64, s & ((1 << 64) - 1)
-    p.inc_hi, p.inc_lo = inc >> 64, inc & ((1 << 64) - 1)
-    p.has_uint32 = int(st["has_uint32"])
-    p.uinteger = int(st["uinteger"])
+        st = g.bit_generator.state
+        s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+        has32, buf = int(st["has_uint32"]), int(st["uinteger"])
+    p.state_hi, p.state_lo = s >> 64, s & _M64
+    p.inc_hi, p.inc_lo = inc >> 64, inc & _M64
+    p.has_uint32 = has32
+    p.uinteger = buf
     return p, warm
 
 
@@ -317,23 +414,39 @@ def collect(raw, jobs, results=None, return_traces: bool = True):
     """Fetch a launch's device outputs and build RunResults (raises on device-side errors)."""
     if results is None:
         results = [None] * len(jobs)
+    import torch
+
     live = raw["live"]
     out = np.frombuffer(raw["out"].cpu().numpy().tobytes(), dtype=np.dtype(
         [("n_reveals", "<i8"), ("iterations", "<i4"), ("terminated_by", "<i4"), ("status", "<i4"), ("pad", "<i4")]))
     topk = raw["topk"].cpu().numpy()
     if return_traces:
-        tr_i, tr_t, tr_v = (raw[k].cpu().numpy() for k in ("tr_i", "tr_t", "tr_v"))
+        # only the used prefix of every run's N*T trace slots crosses PCIe: gather them on the device first
+        nrev = out["n_reveals"].astype(np.int64)
+        starts = np.array([raw["descs"][slot].trace_off for slot in range(len(live))], dtype=np.int64)
+        cum = np.zeros(len(live) + 1, np.int64)
+        np.cumsum(nrev, out=cum[1:])
+        dev = raw["tr_i"].device
+        if int(cum[-1]):
+            shift = torch.from_numpy(np.repeat(starts - cum[:-1], nrev)).to(dev, non_blocking=True)
+            pos = torch.arange(int(cum[-1]), dtype=torch.int64, device=dev) + shift
+            tr_i, tr_t, tr_v = (raw[k][pos].cpu().numpy() for k in ("tr_i", "tr_t", "tr_v"))
+        else:
+            tr_i, tr_t, tr_v = np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.float64)
     for slot, r in enumerate(live):
         job, o, d = jobs[r], out[slot], raw["descs"][slot]
         if o["status"] == 1:
             raise RuntimeError("internal error: both boundary rows exhausted while unseparated")
+        if o["status"] == _lib.CBX_BANDIT_EDESC:
+            raise ValueError(f"run {r}: descriptor outside the kernel's shape contract (n_rows >= 1, "
+                             f"1 <= n_cols <= {MAX_COLS}, 1 <= k <= n_rows)")
         if o["status"] != 0:
             raise RuntimeError(f"bandit kernel status {int(o['status'])} (exact-sum capacity exceeded)")
         nrev = int(o["n_reveals"])
         reveals = []
         if return_traces:
-            a = d.trace_off
-            reveals = list(zip(tr_i[a:a + nrev].tolist(), tr_t[a:a + nrev].tolist(), tr_v[a:a + nrev].tolist()))
+            a, b = int(cum[slot]), int(cum[slot + 1])
+            reveals = Reveals(tr_i[a:b], tr_t[a:b], tr_v[a:b])
         term = "separation" if o["terminated_by"] == _lib.CBX_TERM_SEPARATION else "exhaustion"
         results[r] = RunResult([int(x) for x in topk[slot, : job.cfg.k]], nrev / (job.n_rows * job.n_cols),
                                reveals, int(o["iterations"]), term)

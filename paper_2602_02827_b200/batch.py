@@ -425,6 +425,9 @@ class Corpus:
         ``cand_ids`` [sum N_q] corpus document ids, ``q_cand_off`` [nq + 1] (int64 numpy or CPU tensors).
         ``mode="packed"`` streams the candidates straight from the corpus (tcgen05 path, no copy);
         ``mode="gather"`` first packs them into a contiguous batch (any dtype / path).
+        ``sync=False`` returns at once: the returned pinned tensors are the call's own (later calls never
+        overwrite them) and become valid when the stream reaches them; a bad candidate id is reported by
+        ``synchronize()`` or by the next call.
         """
         import torch
 
@@ -443,10 +446,16 @@ class Corpus:
         # IndexError at the synchronisation below); the gather mode sizes its copy on the host
         if mode == "gather" and n_cand and (cid_np.min() < 0 or cid_np.max() >= self.n_docs):
             raise IndexError(f"candidate id out of range [0, {self.n_docs})")
+        # an asynchronous call (sync=False) must not share pinned staging with a call still in flight: it
+        # takes fresh blocks from torch's caching host allocator (which holds a block until the copies that
+        # used it have completed) and its status is checked at the next synchronisation
+        self._check_pending(wait=sync)
+        pinned = (lambda name, n, dt: self._buf(name, n, dt, pinned=True)) if sync else \
+            (lambda name, n, dt: torch.empty(max(int(n), 1), dtype=dt, pin_memory=True)[:n])
         # host -> device: the call's inputs only
         dq = self._buf("q", q_tokens.numel(), q_tokens.dtype).view(q_tokens.shape)
         dq.copy_(q_tokens, non_blocking=True)
-        hoff = self._buf("hoff", 2 * (nq + 1), torch.int64, pinned=True)
+        hoff = pinned("hoff", 2 * (nq + 1), torch.int64)
         hoff[: nq + 1].copy_(torch.from_numpy(qo))
         hoff[nq + 1:].copy_(torch.from_numpy(co))
         doffs = self._buf("offs", 2 * (nq + 1), torch.int64)
@@ -486,14 +495,40 @@ class Corpus:
                                                  stream), "gather")
             b = TokenBatch(dq, dqo, rows, doff, dco, self.clamp_negative, max_lq, max_nc, total_rows)
             idx, val, _ = rerank_topk(b, k, path)
-        out_i = self._buf("oi", idx.numel(), torch.int32, pinned=True).view(idx.shape)
-        out_v = self._buf("ov", val.numel(), torch.float32, pinned=True).view(val.shape)
+        out_i = pinned("oi", idx.numel(), torch.int32).view(idx.shape)
+        out_v = pinned("ov", val.numel(), torch.float32).view(val.shape)
         out_i.copy_(idx, non_blocking=True)
         out_v.copy_(val, non_blocking=True)
-        st_h = self._buf("st_h", 1, torch.int32, pinned=True)
+        st_h = pinned("st_h", 1, torch.int32)
         st_h.copy_(status, non_blocking=True)  # read back with the outputs: one synchronisation per call
         if sync:
             torch.cuda.current_stream().synchronize()
             if int(st_h[0]):
                 raise IndexError("candidate id out of range")
+        else:
+            ev = torch.cuda.Event()
+            ev.record()
+            self._pending.append((ev, st_h))
         return out_i, out_v
+
+    def _check_pending(self, wait: bool):
+        """Status of earlier sync=False calls: completed ones are checked (all of them when ``wait``)."""
+        pend = getattr(self, "_pending", None)
+        if pend is None:
+            pend = self._pending = []
+        keep = []
+        bad = False
+        for ev, st_h in pend:
+            if wait:
+                ev.synchronize()
+            elif not ev.query():
+                keep.append((ev, st_h))
+                continue
+            bad |= bool(int(st_h[0]))
+        self._pending = keep
+        if bad:
+            raise IndexError("candidate id out of range (in an earlier rerank_topk(sync=False) call)")
+
+    def synchronize(self):
+        """Wait for every rerank_topk(sync=False) call in flight; raises IndexError if one saw a bad candidate id."""
+        self._check_pending(wait=True)

@@ -32,18 +32,37 @@ constexpr int BD_THREADS = 256;
 constexpr int BD_WARPS = BD_THREADS / 32;
 constexpr int BD_CAP = 8;              // exact-sum expansion capacity (CPython fsum partials)
 constexpr int BD_SMEM_ROWS = 2560;     // pools up to this size keep all per-row state in shared memory
-constexpr int BD_MAX_T = 64;
+constexpr int BD_MAX_T = 128;          // query tokens per run (the paper's queries reach 100 tokens)
 constexpr double BD_FX_SCALE = 281474976710656.0;        // 2^48
 constexpr double BD_FX_INV = 1.0 / 281474976710656.0;    // 2^-48
-constexpr double BD_FX_LIMIT = 36028797018963968.0;      // 2^55: 64 terms stay below 2^61
+constexpr double BD_FX_LIMIT = 36028797018963968.0;      // 2^55: 128 terms stay below 2^62
 
 static_assert(sizeof(cbx_bandit_run_desc) == 152, "cbx_bandit_run_desc layout");
 static_assert(sizeof(cbx_bandit_out) == 24, "cbx_bandit_out layout");
+static_assert(BD_MAX_T == CBX_BANDIT_MAX_COLS, "column capacity");
 
 // Persistent exact-sum expansion in global memory.
 struct ExpStore {
   double p[BD_CAP];
   int32_t n, pad;
+};
+
+// The unrevealed columns of a row (up to BD_MAX_T = 128), as two 64-bit words.
+struct ColMask {
+  uint64_t lo, hi;
+  __device__ __forceinline__ bool any() const { return (lo | hi) != 0ull; }
+  __device__ __forceinline__ int count() const { return __popcll(lo) + __popcll(hi); }
+  __device__ __forceinline__ bool test(int t) const { return ((t < 64 ? lo >> t : hi >> (t - 64)) & 1ull) != 0ull; }
+  // lowest set column
+  __device__ __forceinline__ int first() const { return lo ? __ffsll((long long)lo) - 1 : 63 + __ffsll((long long)hi); }
+  // the set column of rank `pos` in ascending order (pos < count())
+  __device__ __forceinline__ int nth(uint32_t pos) const {
+    const uint32_t c = (uint32_t)__popcll(lo);
+    uint64_t m = pos < c ? lo : hi;
+    const uint32_t p = pos < c ? pos : pos - c;
+    for (uint32_t q = 0; q < p; ++q) m &= m - 1;  // drop the lowest p set bits
+    return (pos < c ? -1 : 63) + __ffsll((long long)m);
+  }
 };
 
 // Per-row state, structure of arrays: shared memory for small pools, global otherwise.
@@ -54,7 +73,8 @@ struct RowsView {
   double* mean;        // Welford running mean (oracle.py:307-310)
   double* m2;          // Welford sum of squared deviations
   long long* fx;       // exact sum of revealed values x 2^48 while every value is on that grid
-  uint64_t* unrev;     // bit t set = column t not yet revealed
+  uint64_t* unrev_lo;  // bit t set = column t (< 64) not yet revealed
+  uint64_t* unrev_hi;  // columns 64..127
   int32_t* cnt;        // revealed cells per row
   uint8_t* exp_mode;   // 1: the row's exact sum lives in the global expansion store
   uint8_t* member;     // Top-K membership
@@ -65,13 +85,15 @@ struct RowsView {
     mean = ucb + N;
     m2 = mean + N;
     fx = reinterpret_cast<long long*>(m2 + N);
-    unrev = reinterpret_cast<uint64_t*>(fx + N);
-    cnt = reinterpret_cast<int32_t*>(unrev + N);
+    unrev_lo = reinterpret_cast<uint64_t*>(fx + N);
+    unrev_hi = unrev_lo + N;
+    cnt = reinterpret_cast<int32_t*>(unrev_hi + N);
     exp_mode = reinterpret_cast<uint8_t*>(cnt + N);
     member = exp_mode + N;
   }
+  __device__ __forceinline__ ColMask unrev(int i) const { return ColMask{unrev_lo[i], unrev_hi[i]}; }
 };
-constexpr size_t ROW_BYTES = 7 * 8 + 4 + 1 + 1;
+constexpr size_t ROW_BYTES = 8 * 8 + 4 + 1 + 1;
 // tournament-tree nodes get 4 bytes per row (+ CBX_BANDIT_ROW_SLACK rows of slack per run)
 constexpr size_t ROW_STRIDE = ROW_BYTES + 4;
 constexpr int BD_ROW_SLACK = 64;
@@ -713,6 +735,21 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
   const int N = R.n_rows, TC = R.n_cols, K = R.k;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = tid / G, sub = tid % G;
+  // descriptors live in device memory, so the C ABI cannot check them on the host: a run outside the
+  // kernel's shape contract reports CBX_BANDIT_EDESC instead of overrunning its masks and tables
+  if (N < 1 || TC < 1 || TC > BD_MAX_T || K < 1 || K > N || K > P.max_k) {
+    if (tid == 0) {
+      cbx_bandit_out o;
+      o.n_reveals = 0;
+      o.iterations = 0;
+      o.terminated_by = CBX_TERM_SEPARATION;
+      o.status = CBX_BANDIT_EDESC;
+      o.pad = 0;
+      P.out[blockIdx.x] = o;
+      if (P.shard) P.step->phase = CBX_SHARD_DONE;
+    }
+    return;
+  }
   // UNI: every run of the launch has uniform (generic) bounds, so the per-cell-bound code compiles away
   // (a smaller hot loop: measured 2-4 % faster on cfg2/3/5)
   const bool uniform = UNI || R.bounds_off < 0;
@@ -829,7 +866,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
     BD_PHASE(10);
     rv.mean[i] = mean;
     rv.m2[i] = m2;
-    rv.unrev[i] &= ~(1ull << t);
+    if (t < 64) rv.unrev_lo[i] &= ~(1ull << t);
+    else rv.unrev_hi[i] &= ~(1ull << (t - 64));
     rv.cnt[i] = n;
     double lo_sum, hi_sum;
     if (uniform) {
@@ -930,13 +968,15 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
     sq_rho[n] = b;
   }
   __syncthreads();
-  const uint64_t full_mask = TC >= 64 ? ~0ull : ((1ull << TC) - 1ull);
+  const uint64_t full_lo = TC >= 64 ? ~0ull : ((1ull << TC) - 1ull);
+  const uint64_t full_hi = TC >= 128 ? ~0ull : (TC <= 64 ? 0ull : ((1ull << (TC - 64)) - 1ull));
   for (int i = resume ? N : tid; i < N; i += BD_THREADS) {
     rv.mean[i] = 0.0;
     rv.m2[i] = 0.0;
     rv.fx[i] = 0;
     rv.exp_mode[i] = 0;
-    rv.unrev[i] = full_mask;
+    rv.unrev_lo[i] = full_lo;
+    rv.unrev_hi[i] = full_hi;
     rv.cnt[i] = 0;
     double lo_sum, hi_sum;
     if (uniform) {
@@ -1035,7 +1075,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
     BD_PHASE(0);
     if (warp == 0) {
       int wsel_i = -1;
-      uint64_t wsel_un = 0;
+      ColMask wsel_un{0ull, 0ull};
       Cand f[4];
       if (use_tree) {
 #pragma unroll
@@ -1057,7 +1097,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
         const double ucb_minus = i_minus >= 0 ? ord_val(f[1].key) : -INFINITY;
         // everything else the decision may read, issued together (one round trip when rows live in HBM)
         const double ucb_p = rv.ucb[i_plus], lcb_m = rv.lcb[im];
-        const uint64_t un_p = rv.unrev[i_plus], un_m = rv.unrev[im];
+        const ColMask un_p = rv.unrev(i_plus), un_m = rv.unrev(im);
         int action;
         if (lcb_plus >= ucb_minus) {
           action = 1;
@@ -1071,11 +1111,11 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
           const double wp = __dsub_rn(ucb_p, lcb_plus);
           const double wm = __dsub_rn(ucb_minus, lcb_m);
           int i_star = wp >= wm ? i_plus : i_minus;
-          uint64_t un = i_star == i_plus ? un_p : un_m;
-          if (!un) {
+          ColMask un = i_star == i_plus ? un_p : un_m;
+          if (!un.any()) {
             i_star = i_star == i_plus ? i_minus : i_plus;
             un = i_star == i_plus ? un_p : un_m;
-            if (!un) {
+            if (!un.any()) {
               action = 4;
               ctrl->status = 1;
             }
@@ -1083,12 +1123,9 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
           if (action == 0) {
             int t_star;
             if (rng.random() < eps) {
-              uint32_t pos = rng.integers((uint32_t)__popcll(un));
-              uint64_t m = un;
-              for (uint32_t q = 0; q < pos; ++q) m &= m - 1;  // drop the lowest `pos` set bits
-              t_star = __ffsll((long long)m) - 1;
+              t_star = un.nth(rng.integers((uint32_t)un.count()));
             } else if (uniform) {
-              t_star = __ffsll((long long)un) - 1;  // all widths equal: first unrevealed column
+              t_star = un.first();  // all widths equal: first unrevealed column
             } else {
               // first argmax of the width over the ascending unrevealed columns: warp 0 below
               t_star = -1;
@@ -1104,13 +1141,13 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
       }
       const int wi = uniform ? -1 : __shfl_sync(0xffffffffu, wsel_i, 0);
       if (wi >= 0) {  // one column per lane, warp argmax, ties to the lowest column (select_token, bandit.py:116-136)
-        const uint64_t un = __shfl_sync(0xffffffffu, wsel_un, 0);
+        const ColMask un{__shfl_sync(0xffffffffu, wsel_un.lo, 0), __shfl_sync(0xffffffffu, wsel_un.hi, 0)};
         Cand c{0, TIE_EMPTY};
         for (int t = lane; t < TC; t += 32)
-          if ((un >> t) & 1ull)
+          if (un.test(t))
             cand_take(c, ord_key(__dsub_rn(hi_b[(int64_t)wi * TC + t], lo_b[(int64_t)wi * TC + t])), (uint32_t)t);
         c = warp_best(c);
-        if (lane == 0) ctrl->t_star = c.key ? (int)c.tie : __ffsll((long long)un) - 1;
+        if (lane == 0) ctrl->t_star = c.key ? (int)c.tie : un.first();
       }
     }
     __syncthreads();
@@ -1389,6 +1426,33 @@ __global__ void __launch_bounds__(256) warm_cells_kernel(const BanditParams P, i
   }
 }
 
+// numpy PCG64 stream check (cbx_pcg64_draws): one thread replays a list of draws with the loop's generator
+__global__ void pcg64_draws_kernel(cbx_pcg64 st, const uint32_t* __restrict__ ops, int64_t n_ops, uint64_t* out,
+                                   cbx_pcg64* st_out) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  Pcg64 rng;
+  rng.sh = st.state_hi;
+  rng.sl = st.state_lo;
+  rng.ih = st.inc_hi;
+  rng.il = st.inc_lo;
+  rng.has32 = st.has_uint32;
+  rng.buf = st.uinteger;
+  for (int64_t j = 0; j < n_ops; ++j) {
+    const uint32_t n = ops[j];
+    out[j] = n == 0 ? (uint64_t)__double_as_longlong(rng.random()) : (uint64_t)rng.integers(n);
+  }
+  if (st_out) {
+    cbx_pcg64 o;
+    o.state_hi = rng.sh;
+    o.state_lo = rng.sl;
+    o.inc_hi = rng.ih;
+    o.inc_lo = rng.il;
+    o.has_uint32 = rng.has32;
+    o.uinteger = rng.buf;
+    *st_out = o;
+  }
+}
+
 }  // namespace cbx
 
 using namespace cbx;
@@ -1452,6 +1516,15 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
 extern "C" {
 
 void cbx_bandit_set_profile(void* counters) { g_bandit_prof = static_cast<unsigned long long*>(counters); }
+
+int cbx_pcg64_draws(const cbx_pcg64* state, const uint32_t* ops, int64_t n_ops, uint64_t* out, cbx_pcg64* state_out,
+                    void* stream) {
+  if (!state || (n_ops > 0 && (!ops || !out))) return fail(CBX_EINVAL, "pcg64_draws: NULL buffer");
+  if (n_ops < 0) return fail(CBX_EINVAL, "pcg64_draws: negative draw count");
+  pcg64_draws_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(*state, ops, n_ops, out, state_out);
+  CBX_LAUNCH_CHECK("pcg64_draws_kernel launch");
+  return CBX_OK;
+}
 
 size_t cbx_bandit_state_bytes(int64_t total_rows) {
   size_t a, b, c, d;
@@ -1590,6 +1663,9 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
   P.own_hi = sa ? sa->own_hi : 0;
   P.xchg = sa ? sa->xchg : nullptr;
   P.step = sa ? static_cast<BdStep*>(sa->step) : nullptr;
+  // widest run of the launch (sizes the per-cell bounds staged in shared memory): the batch's longest query,
+  // or the matrix width
+  const int64_t max_t = std::min<int64_t>(BD_MAX_T, b ? std::max(b->max_lq, 1) : std::max<int64_t>(ld_matrix, 1));
   size_t smem = 128 + sizeof(Cand) * 4 * 16 + 2 * sizeof(double) * (BD_MAX_T + 1);  // reductions: up to 16 warps
   smem = align_up(smem, 16);
   P.use_smem = (max_rows <= BD_SMEM_ROWS && !sa) ? 1 : 0;  // a sharded run resumes from global state
@@ -1612,9 +1688,9 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
   P.bounds_smem = 0;
   P.bounds_smem_off = 0;
   if (!sa && CBX_BD_WIDE && n_runs <= sm_count() && max_rows <= BD_SMEM_ROWS) {
-    // 3 expansions per row, plus lo/hi for up to BD_MAX_T columns per row when per-cell bounds are given
+    // 3 expansions per row, plus lo/hi for up to max_t columns per row when per-cell bounds are given
     const size_t need = (size_t)max_rows * 3 * sizeof(ExpStore) +
-                        (bounds_lo ? (size_t)max_rows * BD_MAX_T * 2 * sizeof(double) : 0);
+                        (bounds_lo ? (size_t)max_rows * max_t * 2 * sizeof(double) : 0);
     const size_t off = align_up(smem, 16);
     if (off + need <= 220 * 1024) {
       P.bounds_smem = 1;

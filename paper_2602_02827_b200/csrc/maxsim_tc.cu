@@ -38,6 +38,11 @@ constexpr int TC_EPI_WARP0 = CBX_TC_EPI_WARP0;
 static_assert(TC_EPI_WARP0 % 4 == 0, "epilogue warps must cover TMEM lane quarters 0..3 in order");
 constexpr int TC_ACC_BUFS = 4;
 constexpr int TC_MAX_TILE_N = 128;
+#ifndef CBX_PK_TILE_N
+#define CBX_PK_TILE_N 128  // packed-mode tile height (build knob; 64 measured much slower)
+#endif
+static_assert(CBX_PK_TILE_N == 32 || CBX_PK_TILE_N == 64 || CBX_PK_TILE_N == 128,
+              "packed tile height must be 32, 64 or 128 rows (8-row TMA boxes d[k8], whole pack slots)");
 constexpr int TC_MAX_STAGES = 8;
 #ifndef CBX_PACK_ALIGN
 #define CBX_PACK_ALIGN 32
@@ -47,6 +52,8 @@ constexpr int TC_MAX_STAGES = 8;
 #endif
 static_assert(CBX_PK_PRODUCERS >= 1 && CBX_PK_PRODUCERS <= CBX_TC_EPI_WARP0 - 1, "producers must end before the epilogue");
 constexpr int TC_PACK = CBX_PACK_ALIGN;  // packed-mode row granularity (power of two, >= 8)
+static_assert(TC_PACK >= 8 && (TC_PACK & (TC_PACK - 1)) == 0 && CBX_PK_TILE_N % TC_PACK == 0,
+              "packed tiles must hold whole pack slots");
 
 struct TcParams {
   const int64_t* q_tok_off;
@@ -729,7 +736,7 @@ static int prepare_tc(const cbx_batch* b, const void* d_rows, int64_t n_rows, fl
   p.doc_len = nullptr;
   p.n_tokens_dev = nullptr;
   p.ilv = 0;
-  p.k8 = tile_n == 128 ? 4 : tile_n == 64 ? 3 : 2;  // d[k8] = 8-row boxes
+  p.k8 = 31 - __builtin_clz((unsigned)(tile_n / 8));  // d[k8] = 8-row boxes (tile_n >> k8 == 8)
   p.corpus_rows = n_rows;
   p.n_queries = b->n_queries;
   p.n_docs = b->n_docs;
@@ -790,9 +797,6 @@ int launch_maxsim_tc_packed(const cbx_batch* b, const int64_t* corpus_off, int64
   plan_add_kernel<<<(unsigned)nb, PL_THREADS, 0, stream>>>(pk, n, btot, nb);
   CBX_LAUNCH_CHECK("plan_add_kernel launch");
   TcLaunch L;
-#ifndef CBX_PK_TILE_N
-#define CBX_PK_TILE_N 128
-#endif
   int rc = prepare_tc(b, b->d_tokens, b->n_d_tokens, scores, L, CBX_PK_TILE_N);
   if (rc) return rc;
   L.p.packed = 1;

@@ -32,6 +32,9 @@ __all__ = [
     "CONFIGS",
     "QueryCase",
     "gen_query",
+    "gen_batch_device",
+    "batch_plan",
+    "query_blocks",
     "to_float64",
     "bf16_bits_from_f32",
     "bf16_bits_to_f32",
@@ -191,30 +194,18 @@ def gen_query(cfg: WorkloadConfig | str, q: int = 0, n_docs: int | None = None) 
     return QueryCase(cfg, _cast(query, cfg.dtype), _cast(tokens, cfg.dtype), offsets, relevant)
 
 
-def gen_batch_device(cfg: WorkloadConfig | str, n_queries: int | None = None, seed: int = 0, device="cuda",
-                     n_docs: int | None = None):
-    """Draw a whole batch of a config directly in HBM with torch's device RNG.
-
-    Same recipe as :func:`gen_query` (unit Gaussian tokens, planted /
-    clustered relevance, lognormal or fixed lengths) but a different random
-    stream: parity against the oracle is done on device->host copies.
-    Returns ``(TokenBatch, host_offsets)`` with host copies of the offsets.
-    """
+def batch_plan(cfg: WorkloadConfig | str, n_queries: int | None = None, seed: int = 0, n_docs: int | None = None):
+    """Host side of :func:`gen_batch_device` for the WHOLE batch: per-query lengths (doc lengths [nq, n] and
+    query lengths [nq]) from one host generator, so every rank of a sharded run agrees on every query's shape
+    and can cut the batch into balanced query blocks before drawing any token."""
     import torch
-
-    from .batch import TokenBatch
 
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
     nq = cfg.n_queries if n_queries is None else int(n_queries)
     n = cfg.n_docs if n_docs is None else int(n_docs)
-    d = cfg.dim
-    tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[cfg.dtype]
-    g = torch.Generator(device=device)
-    g.manual_seed(int(seed) * 1_000_003 + cfg.seed)
     gc = torch.Generator()
     gc.manual_seed(int(seed) * 1_000_003 + cfg.seed)
-    # lengths and query lengths on the host generator (small)
     kind, a, b, c = cfg.doc_len
     if kind == "uniform":
         lens = torch.randint(int(a), int(b) + 1, (nq * n,), generator=gc)
@@ -225,45 +216,98 @@ def gen_batch_device(cfg: WorkloadConfig | str, n_queries: int | None = None, se
     else:
         lens = torch.full((nq * n,), int(a), dtype=torch.int64)
     lqs = torch.randint(cfg.lq[0], cfg.lq[1] + 1, (nq,), generator=gc)
-    d_off = torch.zeros(nq * n + 1, dtype=torch.int64)
-    torch.cumsum(lens, 0, out=d_off[1:])
-    q_off = torch.zeros(nq + 1, dtype=torch.int64)
-    torch.cumsum(lqs, 0, out=q_off[1:])
-    qd_off = torch.arange(0, nq * n + 1, n, dtype=torch.int64)
+    return cfg, lens.numpy().reshape(nq, n), lqs.numpy().astype(np.int64)
+
+
+def query_blocks(lens: np.ndarray, world: int) -> list[tuple[int, int]]:
+    """Contiguous query blocks [a, b) for `world` ranks, balanced by doc tokens (the scorer's HBM bytes,
+    sum L_i * d * s per query)."""
+    per_q = np.asarray(lens, dtype=np.int64).reshape(len(lens), -1).sum(axis=1)
+    nq = len(per_q)
+    off = np.zeros(nq + 1, np.int64)
+    np.cumsum(per_q, out=off[1:])
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(int(np.searchsorted(off[:nq], (int(off[-1]) * r) // world, side="left")))
+    cuts.append(nq)
+    cuts = np.maximum.accumulate(np.array(cuts))
+    return [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
+
+
+def gen_batch_device(cfg: WorkloadConfig | str, n_queries: int | None = None, seed: int = 0, device="cuda",
+                     n_docs: int | None = None, queries: tuple[int, int] | None = None):
+    """Draw a batch of a config directly in HBM with torch's device RNG.
+
+    Same recipe as :func:`gen_query` (unit Gaussian tokens, planted /
+    clustered relevance, lognormal or fixed lengths) but a different random
+    stream: parity against the oracle is done on device->host copies.
+    Shapes come from :func:`batch_plan`; query q's tokens are drawn from its
+    own generator (seeded by (seed, cfg, q)), so ``queries=(a, b)`` yields
+    exactly queries a..b-1 of the full batch — what one rank of a
+    query-sharded run holds. Returns ``(TokenBatch, host_offsets)`` with host
+    copies of the (block-local) offsets.
+    """
+    import torch
+
+    from .batch import TokenBatch
+
+    cfg, lens_all, lqs_all = batch_plan(cfg, n_queries, seed, n_docs)
+    nq_all, n = lens_all.shape
+    qa, qb = (0, nq_all) if queries is None else (int(queries[0]), int(queries[1]))
+    if not 0 <= qa <= qb <= nq_all:
+        raise ValueError(f"query block {queries} outside [0, {nq_all}]")
+    nq = qb - qa
+    d = cfg.dim
+    tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[cfg.dtype]
+    lens = lens_all[qa:qb].reshape(-1)
+    lqs = lqs_all[qa:qb]
+    d_off = np.zeros(nq * n + 1, dtype=np.int64)
+    np.cumsum(lens, out=d_off[1:])
+    q_off = np.zeros(nq + 1, dtype=np.int64)
+    np.cumsum(lqs, out=q_off[1:])
+    qd_off = np.arange(0, nq * n + 1, n, dtype=np.int64)
     total = int(d_off[-1])
 
     def unit_rows(x):
         return x / x.norm(dim=-1, keepdim=True)
 
-    q_tokens = unit_rows(torch.randn(int(q_off[-1]), d, device=device, generator=g)).to(tdt)
+    q_tokens = torch.empty(int(q_off[-1]), d, dtype=tdt, device=device)
     d_tokens = torch.empty(total, d, dtype=tdt, device=device)
-    step = 1 << 22
-    for s in range(0, total, step):
-        e = min(total, s + step)
-        d_tokens[s:e] = unit_rows(torch.randn(e - s, d, device=device, generator=g)).to(tdt)
     noise = cfg.planted_sigma / math.sqrt(d)
     n_rel = min(n, int(round(cfg.n_relevant * n / cfg.n_docs))) if cfg.n_relevant else 0
-    if n_rel and cfg.scheme in ("planted", "clustered"):
-        d_off_dev = d_off.to(device)
-        q_off_dev = q_off.to(device)
-        for q in range(nq):
-            rel = torch.randperm(n, generator=gc)[:n_rel] + q * n
-            q_rows = q_tokens[int(q_off[q]):int(q_off[q + 1])].float()
-            lq = q_rows.shape[0]
-            for r in rel.tolist():
-                s0, L = int(d_off[r]), int(lens[r])
-                m = int(round(cfg.planted_frac * L))
-                pos = torch.randperm(L, generator=gc)[:m].to(device) + s0
-                if cfg.scheme == "planted":
-                    ts = torch.randint(0, lq, (m,), generator=gc).to(device)
-                    base = q_rows[ts]
-                else:
-                    ts = torch.randint(0, lq, (8,), generator=gc).to(device)
-                    cent = unit_rows(q_rows[ts] + noise * torch.randn(8, d, device=device, generator=g))
-                    base = cent[torch.randint(0, 8, (m,), generator=gc).to(device)]
-                d_tokens[pos] = unit_rows(base + noise * torch.randn(m, d, device=device, generator=g)).to(tdt)
-        del d_off_dev, q_off_dev
-    host = (q_off.numpy(), d_off.numpy(), qd_off.numpy())
-    batch = TokenBatch.from_device(q_tokens, q_off.to(device), d_tokens, d_off.to(device), qd_off.to(device),
+    step = 1 << 22
+    for qi in range(nq):
+        q = qa + qi
+        qseed = (int(seed) * 1_000_003 + cfg.seed) * 65_537 + q
+        g = torch.Generator(device=device)
+        g.manual_seed(qseed)
+        gc = torch.Generator()
+        gc.manual_seed(qseed)
+        q_rows = unit_rows(torch.randn(int(lqs[qi]), d, device=device, generator=g))
+        q_tokens[int(q_off[qi]):int(q_off[qi + 1])] = q_rows.to(tdt)
+        t0, t1 = int(d_off[qi * n]), int(d_off[(qi + 1) * n])
+        for s0 in range(t0, t1, step):
+            e = min(t1, s0 + step)
+            d_tokens[s0:e] = unit_rows(torch.randn(e - s0, d, device=device, generator=g)).to(tdt)
+        if not (n_rel and cfg.scheme in ("planted", "clustered")):
+            continue
+        q_rows = q_tokens[int(q_off[qi]):int(q_off[qi + 1])].float()
+        lq = q_rows.shape[0]
+        rel = torch.randperm(n, generator=gc)[:n_rel] + qi * n
+        for r in rel.tolist():
+            s0, L = int(d_off[r]), int(lens[r])
+            m = int(round(cfg.planted_frac * L))
+            pos = torch.randperm(L, generator=gc)[:m].to(device) + s0
+            if cfg.scheme == "planted":
+                ts = torch.randint(0, lq, (m,), generator=gc).to(device)
+                base = q_rows[ts]
+            else:
+                ts = torch.randint(0, lq, (8,), generator=gc).to(device)
+                cent = unit_rows(q_rows[ts] + noise * torch.randn(8, d, device=device, generator=g))
+                base = cent[torch.randint(0, 8, (m,), generator=gc).to(device)]
+            d_tokens[pos] = unit_rows(base + noise * torch.randn(m, d, device=device, generator=g)).to(tdt)
+    host = (q_off, d_off, qd_off)
+    batch = TokenBatch.from_device(q_tokens, torch.from_numpy(q_off).to(device), d_tokens,
+                                   torch.from_numpy(d_off).to(device), torch.from_numpy(qd_off).to(device),
                                    clamp_negative=False, host_offsets=host)
     return batch, host

@@ -30,7 +30,7 @@ def test_library_loads_and_exports_every_declared_symbol():
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
     assert set(_lib.SIGNATURES) == set(declared_symbols())
-    assert lib.cbx_abi_version() == 1
+    assert lib.cbx_abi_version() == _lib.CBX_ABI_VERSION == 1
 
 
 def test_struct_layouts_match_the_header():
@@ -75,3 +75,30 @@ def test_product_package_never_imports_the_test_oracle():
             continue
         src = open(os.path.join(pkg, name)).read()
         assert not re.search(r"^\s*(from\s+oracle\b|import\s+oracle\b)", src, flags=re.M), name
+
+
+def test_header_constants_match_the_binding():
+    """Every numeric ``#define CBX_*`` of the header has the same value in the ctypes binding."""
+    src = open(HEADER).read()
+    defs = dict(re.findall(r"^#define\s+(CBX_\w+)\s+(-?\d+)\b", src, flags=re.M))
+    assert "CBX_BANDIT_MAX_COLS" in defs and "CBX_BANDIT_EDESC" in defs
+    missing = [k for k in defs if not hasattr(_lib, k)]
+    assert not missing, missing
+    for k, v in defs.items():
+        assert getattr(_lib, k) == int(v), k
+
+
+def test_experimental_library_override_needs_the_tools_flag():
+    """CBX_LIB alone never redirects the product to another .so (tests, smoke() and bench load the in-tree one)."""
+    import subprocess
+    import sys
+
+    code = ("import os, sys; sys.path.insert(0, %r); from paper_2602_02827_b200 import _lib; print(_lib.LIB_PATH)"
+            % ROOT)
+    env = dict(os.environ, CBX_LIB="/tmp/not_the_product.so")
+    env.pop("CBX_TOOLS", None)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True).stdout
+    assert out.strip() == os.path.join(ROOT, "paper_2602_02827_b200", "libcbx.so")
+    env["CBX_TOOLS"] = "1"
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True).stdout
+    assert out.strip() == "/tmp/not_the_product.so"

@@ -278,3 +278,106 @@ def test_fp32_queries_meet_the_baseline_criterion():
                                        rtol=0, atol=1e-15)
         identical += same_cells
     assert identical >= len(cases) // 2, identical
+
+
+def test_device_pcg64_streams_equal_numpy():
+    """The loop's PCG64 replica (cbx_pcg64_draws) against numpy's streams: random() bit patterns and
+    integers(n) for n up to 2^31, where Lemire's rejection branch runs (golden pcg64_streams.json)."""
+    import ctypes
+
+    from paper_2602_02827_b200 import _lib
+
+    lib = _lib.load()
+    with open(os.path.join(GOLDEN, "pcg64_streams.json")) as f:
+        streams = json.load(f)
+    rejected = 0
+    for s in streams:
+        st, inc = int(s["state"]), int(s["inc"])
+        p = _lib.CbxPcg64(st >> 64, st & (2**64 - 1), inc >> 64, inc & (2**64 - 1), s["has_uint32"], s["uinteger"])
+        ops = np.array([0 if k == "r" else n for k, n, _ in s["ops"]], dtype=np.uint32)
+        d_ops = torch.from_numpy(ops.view(np.int32)).cuda()
+        out = torch.empty(len(ops), dtype=torch.int64, device="cuda")
+        st_out = torch.zeros(ctypes.sizeof(_lib.CbxPcg64), dtype=torch.uint8, device="cuda")
+        _lib.check(lib.cbx_pcg64_draws(ctypes.byref(p), d_ops.data_ptr(), len(ops), out.data_ptr(),
+                                       st_out.data_ptr(), None), "pcg64_draws")
+        got = out.cpu().numpy().view(np.uint64)
+        for (k, n, want), g in zip(s["ops"], got):
+            if k == "r":
+                assert np.uint64(g).view(np.float64) == want
+            else:
+                assert int(g) == want
+                rejected += n > 2**20
+        # the generator state after the stream equals numpy's after the same draws
+        gen = np.random.default_rng(_seed(s["seed"]))
+        for k, n, _ in s["ops"]:
+            gen.random() if k == "r" else gen.integers(n)
+        ref = gen.bit_generator.state
+        o = _lib.CbxPcg64.from_buffer_copy(st_out.cpu().numpy().tobytes())
+        assert (o.state_hi << 64 | o.state_lo) == ref["state"]["state"]
+        assert o.has_uint32 == ref["has_uint32"] and o.uinteger == ref["uinteger"]
+    assert rejected > 100  # large bounds: Lemire's rejection path is exercised
+
+
+def test_device_guard_rejects_descriptors_outside_the_shape_contract():
+    """A C-ABI caller's descriptors live on the device: a run with n_cols > 128 or k > n_rows must report
+    CBX_BANDIT_EDESC (ValueError) instead of overrunning the kernel's column masks."""
+    from paper_2602_02827_b200 import BanditConfig, BanditJob
+    from paper_2602_02827_b200.bandit import collect, launch_batch, prepare_batch
+
+    m = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, (20, 8))).cuda()
+    for field_off, bad in ((20, 200), (24, 21)):  # n_cols = 200; k = 21 > n_rows
+        jobs = [BanditJob(BanditConfig(k=3, seed=1), 20, 8, 0, 0, (-1.0, 1.0))]
+        p = prepare_batch(jobs, matrix=m)
+        raw_desc = p["desc_t"].cpu().numpy().copy()
+        raw_desc[field_off:field_off + 4] = np.frombuffer(np.int32(bad).tobytes(), np.uint8)
+        p["desc_t"] = torch.from_numpy(raw_desc).cuda()
+        with pytest.raises(ValueError, match="shape contract"):
+            collect(launch_batch(p), jobs, list(p["results"]))
+
+
+def test_wide_queries_up_to_128_tokens_match_the_oracle():
+    """Lq up to 128 (the paper's multimodal queries reach 100 tokens): matrix-backed random cases with
+    uniform and per-cell bounds, and a token-backed pool with 100-token queries, against the oracle."""
+    from paper_2602_02827_b200 import BanditConfig, BanditJob, CellBounds, MaxSimOracle, run, run_batch
+    from paper_2602_02827_b200.batch import TokenBatch
+
+    rng = np.random.default_rng(128)
+    for it in range(12):
+        n, t = int(rng.integers(3, 50)), int(rng.integers(65, 129))
+        matrix = rng.uniform(-0.2, 1.0, size=(n, t))
+        if it % 2:
+            lo, hi = np.full((n, t), -0.2), np.full((n, t), 1.0)
+        else:
+            lo = matrix - rng.uniform(0.0, 0.4, size=(n, t))
+            hi = matrix + rng.uniform(0.0, 0.4, size=(n, t))
+        mode = ("epsilon-greedy", "static-warmup", "uniform-row")[it % 3]
+        kw = dict(k=int(rng.integers(1, n + 1)), alpha_ef=float(rng.choice([1.0, 0.3, 0.05])),
+                  epsilon=float(rng.choice([0.0, 0.1, 0.5])), explore_mode=mode,
+                  gamma_init=0.2 if mode == "static-warmup" else 0.0, seed=(5, it))
+        got = run(MaxSimOracle.from_matrix(matrix, value_range=(-0.7, 1.5)), CellBounds(lo, hi), BanditConfig(**kw))
+        ref = bandit_ref.run(matrix, lo, hi, **kw)
+        assert got.reveals == ref.reveals and got.topk == ref.topk and got.iterations == ref.iterations
+    # token-backed: 100-token bf16 queries over 60-doc pools (cells computed on demand in the kernel)
+    cases = []
+    for q in range(3):
+        g = np.random.default_rng((100, q))
+        qv = g.standard_normal((100, 128))
+        qv /= np.linalg.norm(qv, axis=1, keepdims=True)
+        lens = g.integers(20, 120, size=60)
+        toks = g.standard_normal((int(lens.sum()), 128))
+        toks /= np.linalg.norm(toks, axis=1, keepdims=True)
+        off = np.concatenate([[0], np.cumsum(lens)])
+        qb, tb = W.bf16_bits_from_f32(qv.astype(np.float32)), W.bf16_bits_from_f32(toks.astype(np.float32))
+        cases.append((qb, tb, off))
+    from paper_2602_02827_b200.batch import to_torch_tokens
+
+    b = TokenBatch.from_host([to_torch_tokens(c[0], "bf16") for c in cases],
+                             [[to_torch_tokens(c[1][c[2][i]:c[2][i + 1]], "bf16") for i in range(60)] for c in cases])
+    jobs = [BanditJob(BanditConfig(k=5, alpha_ef=0.2, seed=(0, q)), 60, 100, q, 60 * q, (-1.0, 1.0))
+            for q in range(3)]
+    got = run_batch(jobs, batch=b)
+    for q, (qb, tb, off) in enumerate(cases):
+        t64 = W.to_float64(tb, "bf16")
+        cells = maxsim_ref.cell_matrix(W.to_float64(qb, "bf16"), [t64[off[i]:off[i + 1]] for i in range(60)])
+        ref = bandit_ref.run(cells, -1.0, 1.0, 5, alpha_ef=0.2, seed=(0, q))
+        assert got[q].reveals == ref.reveals and got[q].topk == ref.topk

@@ -1,6 +1,6 @@
 """A/B of the packed (resident-corpus) scorer: parity against the contiguous tcgen05 batch and timing.
 
-Run once per libcbx build (CBX_LIB=...); prints one JSON line: packed scores bit-equal to the contiguous
+Run once per libcbx build (CBX_TOOLS=1 CBX_LIB=...); prints one JSON line: packed scores bit-equal to the contiguous
 scorer on the same candidates, device ms of the packed rerank call and e2e (host in / host out) ms.
 """
 import json
