@@ -284,18 +284,57 @@ def _warms_up(job: BanditJob, uniform) -> bool:
     return bool(lcb_plus < ucb_minus - 1e-9 * (abs(lcb_plus) + abs(ucb_minus) + 1.0))
 
 
+def _desc_dtype() -> np.dtype:
+    """numpy view of cbx_bandit_run_desc (field offsets taken from the ctypes mirror of the header)."""
+    names, formats, offsets = [], [], []
+    for name, ct in _lib.CbxBanditRunDesc._fields_:
+        off = getattr(_lib.CbxBanditRunDesc, name).offset
+        if name == "rng":
+            for sub, sct in _lib.CbxPcg64._fields_:
+                names.append("rng_" + sub)
+                formats.append(np.dtype(sct))
+                offsets.append(off + getattr(_lib.CbxPcg64, sub).offset)
+            continue
+        names.append(name)
+        formats.append(np.dtype(ct))
+        offsets.append(off)
+    return np.dtype({"names": names, "formats": formats, "offsets": offsets,
+                     "itemsize": ctypes.sizeof(_lib.CbxBanditRunDesc)})
+
+
+_DESC_DTYPE = None
+_LOG_TERM_CACHE: dict = {}
+
+
+def _log_term(cfg: BanditConfig, N: int, T: int) -> float:
+    key = (cfg.delta, cfg.c, cfg.union_mode, cfg.alpha_ef, N, T)
+    v = _LOG_TERM_CACHE.get(key)
+    if v is None:
+        if len(_LOG_TERM_CACHE) > 65536:
+            _LOG_TERM_CACHE.clear()
+        v = _LOG_TERM_CACHE[key] = cfg.radius_config.log_term(N, T)
+    return v
+
+
 def prepare_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, prewarm: bool | None = None) -> dict:
     """Host side of a batched launch: validate the jobs, seed the generators, build the run descriptors and
     move them (and any per-cell bounds) to the device; outputs are allocated. ``launch_batch`` then issues
     the kernels. ``prewarm`` (None = auto: when the runs fit one CTA per SM) computes the warm-up cells of
     token-backed runs with one HBM-bound cbx_bandit_prewarm launch ahead of the loop kernel (same values,
-    same traces)."""
+    same traces). The descriptors are filled column-wise into a numpy view of cbx_bandit_run_desc (one
+    host->device copy), so preparing a few hundred runs costs well under the kernel's time."""
+    global _DESC_DTYPE
     torch = _lib.require_cuda()
     lib = _lib.load()
     if batch is None and matrix is None:
         raise ValueError("need a TokenBatch or a device matrix as the cell source")
+    if _DESC_DTYPE is None:
+        _DESC_DTYPE = _desc_dtype()
     n = len(jobs)
-    descs = (_lib.CbxBanditRunDesc * max(n, 1))()
+    cols = {k: [] for k in ("query", "row_begin", "n_rows", "n_cols", "k", "explore_mode", "n_warm", "flags",
+                            "warm_off", "alpha_ef", "epsilon", "log_term", "bounds_off", "lo_uniform", "hi_uniform",
+                            "trace_off", "state_off")}
+    rngs = []
     lo_parts, hi_parts, warm_parts = [], [], []
     b_off = w_off = tr_off = st_off = 0
     max_rows = max_k = 1
@@ -316,44 +355,60 @@ def prepare_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, prewarm: b
         if cfg.k == 0:
             results[r] = RunResult([], 0.0, [], 0, "separation")
             continue
-        d = descs[len(live)]
+        if job.selection not in ("auto", "scan", "tree"):
+            raise ValueError(f"selection must be 'auto', 'scan' or 'tree', got {job.selection!r}")
         live.append(r)
-        d.query, d.row_begin, d.n_rows, d.n_cols, d.k = job.query, job.row_begin, N, T, cfg.k
-        d.explore_mode = _MODE_CODE[cfg.explore_mode]
-        d.alpha_ef, d.epsilon = cfg.alpha_ef, cfg.epsilon
-        d.log_term = cfg.radius_config.log_term(N, T)
+        cols["query"].append(job.query)
+        cols["row_begin"].append(job.row_begin)
+        cols["n_rows"].append(N)
+        cols["n_cols"].append(T)
+        cols["k"].append(cfg.k)
+        cols["explore_mode"].append(_MODE_CODE[cfg.explore_mode])
+        cols["alpha_ef"].append(cfg.alpha_ef)
+        cols["epsilon"].append(cfg.epsilon)
+        cols["log_term"].append(_log_term(cfg, N, T))
         bnd = job.bounds
         uni = bnd if isinstance(bnd, tuple) else bnd.uniform_values()
         if uni:
-            d.bounds_off = -1
-            d.lo_uniform, d.hi_uniform = uni
+            cols["bounds_off"].append(-1)
+            cols["lo_uniform"].append(uni[0])
+            cols["hi_uniform"].append(uni[1])
         else:
-            d.bounds_off = b_off
+            cols["bounds_off"].append(b_off)
+            cols["lo_uniform"].append(0.0)
+            cols["hi_uniform"].append(0.0)
             lo_parts.append(np.ascontiguousarray(bnd.lo, dtype=np.float64).ravel())
             hi_parts.append(np.ascontiguousarray(bnd.hi, dtype=np.float64).ravel())
             b_off += N * T
-        d.rng, warm = _rng_state(cfg.seed, cfg.explore_mode, cfg.gamma_init, N * T)
-        d.n_warm, d.warm_off = len(warm), w_off
+        p, warm = _rng_state(cfg.seed, cfg.explore_mode, cfg.gamma_init, N * T)
+        rngs.append((p.state_hi, p.state_lo, p.inc_hi, p.inc_lo, p.has_uint32, p.uinteger))
+        cols["n_warm"].append(len(warm))
+        cols["warm_off"].append(w_off)
         warm_parts.append(warm)
         w_off += len(warm)
-        if job.selection not in ("auto", "scan", "tree"):
-            raise ValueError(f"selection must be 'auto', 'scan' or 'tree', got {job.selection!r}")
         tree = job.selection == "tree" or (job.selection == "auto" and N > TREE_ROWS)
-        d.flags = _lib.CBX_BANDIT_TREE if tree else 0
+        flags = _lib.CBX_BANDIT_TREE if tree else 0
         pre = prewarm_on and batch is not None and _warms_up(job, uni)
         if pre:
-            d.flags |= _lib.CBX_BANDIT_PREWARMED
+            flags |= _lib.CBX_BANDIT_PREWARMED
+        cols["flags"].append(flags)
         warm_counts.append((N if cfg.explore_mode == "epsilon-greedy" else len(warm)) if pre else 0)
-        d.trace_off, d.state_off = tr_off, st_off
+        cols["trace_off"].append(tr_off)
+        cols["state_off"].append(st_off)
         tr_off += N * T
         st_off += N + _lib.CBX_BANDIT_ROW_SLACK
         max_rows, max_k = max(max_rows, N), max(max_k, cfg.k)
     nl = len(live)
     if nl == 0:
         return dict(results=results, live=live)
+    descs = np.zeros(nl, dtype=_DESC_DTYPE)
+    for k, v in cols.items():
+        descs[k] = v
+    rng_a = np.array(rngs, dtype=np.uint64)
+    for j, sub in enumerate(("state_hi", "state_lo", "inc_hi", "inc_lo", "has_uint32", "uinteger")):
+        descs["rng_" + sub] = rng_a[:, j]
     dev = torch.device("cuda", torch.cuda.current_device())
-    desc_t = torch.frombuffer(bytearray(bytes(descs)[: nl * ctypes.sizeof(_lib.CbxBanditRunDesc)]),
-                              dtype=torch.uint8).to(dev)
+    desc_t = torch.from_numpy(descs.view(np.uint8).reshape(-1)).to(dev)
     lo_t = torch.from_numpy(np.concatenate(lo_parts)).to(dev) if lo_parts else None
     hi_t = torch.from_numpy(np.concatenate(hi_parts)).to(dev) if hi_parts else None
     warm_t = torch.from_numpy(np.concatenate(warm_parts)).to(dev) if w_off else None
@@ -423,7 +478,7 @@ def collect(raw, jobs, results=None, return_traces: bool = True):
     if return_traces:
         # only the used prefix of every run's N*T trace slots crosses PCIe: gather them on the device first
         nrev = out["n_reveals"].astype(np.int64)
-        starts = np.array([raw["descs"][slot].trace_off for slot in range(len(live))], dtype=np.int64)
+        starts = np.asarray(raw["descs"]["trace_off"], dtype=np.int64)
         cum = np.zeros(len(live) + 1, np.int64)
         np.cumsum(nrev, out=cum[1:])
         dev = raw["tr_i"].device
@@ -434,7 +489,7 @@ def collect(raw, jobs, results=None, return_traces: bool = True):
         else:
             tr_i, tr_t, tr_v = np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.float64)
     for slot, r in enumerate(live):
-        job, o, d = jobs[r], out[slot], raw["descs"][slot]
+        job, o = jobs[r], out[slot]
         if o["status"] == 1:
             raise RuntimeError("internal error: both boundary rows exhausted while unseparated")
         if o["status"] == _lib.CBX_BANDIT_EDESC:

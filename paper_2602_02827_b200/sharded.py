@@ -29,7 +29,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .bandit import _MODE_CODE, MAX_COLS, TREE_ROWS, BanditConfig, RunResult, _rng_state
+from .bandit import _MODE_CODE, MAX_COLS, TREE_ROWS, BanditConfig, Reveals, RunResult, _rng_state
 from .bounds import CellBounds
 
 __all__ = ["ShardedBanditRun", "drive", "allreduce_exchange", "shard_batch", "xchg_key", "xchg_value",
@@ -169,8 +169,7 @@ class ShardedBanditRun:
         if out["status"] != 0:
             raise RuntimeError(f"bandit kernel status {int(out['status'])} (exact-sum capacity exceeded)")
         n = int(out["n_reveals"])
-        reveals = list(zip(self._tr_i[:n].cpu().tolist(), self._tr_t[:n].cpu().tolist(),
-                           self._tr_v[:n].cpu().tolist()))
+        reveals = Reveals(self._tr_i[:n].cpu().numpy(), self._tr_t[:n].cpu().numpy(), self._tr_v[:n].cpu().numpy())
         term = "separation" if out["terminated_by"] == _lib.CBX_TERM_SEPARATION else "exhaustion"
         return RunResult([int(x) for x in self._topk.cpu().tolist()], n / (self.n_rows * self.n_cols), reveals,
                          int(out["iterations"]), term)

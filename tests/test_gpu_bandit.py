@@ -97,21 +97,22 @@ def test_token_backed_runs_match_reference_trace_for_trace():
         assert len(full.reveals) == case["full_rerank"]["n_reveals"]
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5"])
-def test_config_query_bandit_matches_reference(name):
-    """One full-shape query of each BASELINE config; cfg5 sweeps all five alphas."""
+@pytest.mark.parametrize("name,q", [("cfg1", 0), ("cfg2", 0), ("cfg2", 1), ("cfg2", 2), ("cfg3", 0), ("cfg3", 1),
+                                    ("cfg5", 0), ("cfg5", 1)])
+def test_config_query_bandit_matches_reference(name, q):
+    """Full-shape queries of each BASELINE config (seed (0, q)); cfg5 sweeps all five alphas."""
     from paper_2602_02827_b200 import BanditConfig, BanditJob, run_batch
     from helpers import batch_of_cases
 
-    path = os.path.join(GOLDEN, f"{name}_q0.npz")
+    path = os.path.join(GOLDEN, f"{name}_q{q}.npz")
     if not os.path.exists(path):
         pytest.skip("fixture missing")
     z = np.load(path)
     cfg = W.CONFIGS[name]
-    case = W.gen_query(name, 0)
+    case = W.gen_query(name, q)
     b = batch_of_cases([case])
     lq = case.query.shape[0]
-    jobs = [BanditJob(BanditConfig(k=cfg.k, alpha_ef=a, seed=(0, 0)), case.n_docs, lq, 0, 0, (-1.0, 1.0))
+    jobs = [BanditJob(BanditConfig(k=cfg.k, alpha_ef=a, seed=(0, q)), case.n_docs, lq, 0, 0, (-1.0, 1.0))
             for a in cfg.alphas]
     results = run_batch(jobs, batch=b)
     for ai, res in enumerate(results):

@@ -74,16 +74,20 @@ def test_scores_and_topk_match_reference_golden(path):
         assert topk_matches(idx[0].tolist(), topk, scores, rtol)
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5"])
-def test_config_query_matches_reference_golden(name):
+CONFIG_FIXTURES = [("cfg1", 0), ("cfg2", 0), ("cfg2", 1), ("cfg2", 2), ("cfg3", 0), ("cfg3", 1), ("cfg5", 0),
+                   ("cfg5", 1)]
+
+
+@pytest.mark.parametrize("name,q", CONFIG_FIXTURES)
+def test_config_query_matches_reference_golden(name, q):
     from paper_2602_02827_b200.batch import rerank_topk
 
-    path = os.path.join(GOLDEN, f"{name}_q0.npz")
+    path = os.path.join(GOLDEN, f"{name}_q{q}.npz")
     if not os.path.exists(path):
         pytest.skip("fixture missing")
     z = np.load(path)
     cfg = W.CONFIGS[name]
-    case = W.gen_query(name, 0)
+    case = W.gen_query(name, q)
     b = batch_of_cases([case])
     idx, val, got = rerank_topk(b, cfg.k)
     rtol = 1e-5 if cfg.dtype == "f32" else 1e-3

@@ -37,3 +37,25 @@ def test_static_warmup_state_follows_the_choice_draw():
     assert warm.tolist() == cells.tolist()
     assert (p.state_hi << 64 | p.state_lo) == st["state"]["state"]
     assert p.has_uint32 == st["has_uint32"] and p.uinteger == st["uinteger"]
+
+
+def test_numpy_descriptor_view_matches_the_ctypes_struct():
+    """prepare_batch fills cbx_bandit_run_desc column-wise through a numpy view: same bytes as ctypes."""
+    from paper_2602_02827_b200 import _lib
+    from paper_2602_02827_b200.bandit import _desc_dtype
+
+    dt = _desc_dtype()
+    assert dt.itemsize == 152
+    d = _lib.CbxBanditRunDesc()
+    a = np.zeros(1, dtype=dt)
+    vals = dict(query=7, row_begin=123456789012, n_rows=1000, n_cols=100, k=10, explore_mode=2, n_warm=5, flags=3,
+                warm_off=99, alpha_ef=0.178, epsilon=0.1, log_term=12.5, bounds_off=-1, lo_uniform=-1.0,
+                hi_uniform=1.0, trace_off=2 ** 40, state_off=2 ** 33)
+    for k, v in vals.items():
+        setattr(d, k, v)
+        a[k] = v
+    rng = (2 ** 63 + 5, 17, 2 ** 64 - 1, 3, 1, 2 ** 32 - 2)
+    d.rng = _lib.CbxPcg64(*rng)
+    for sub, v in zip(("state_hi", "state_lo", "inc_hi", "inc_lo", "has_uint32", "uinteger"), rng):
+        a["rng_" + sub] = v
+    assert a.tobytes() == bytes(d)

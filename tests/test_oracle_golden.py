@@ -143,15 +143,16 @@ def test_bound_scalars_frozen_values():
 
 
 # ---------------------------------------------------------------- full-shape configs
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5"])
-def test_config_fixture_fingerprint_and_p1(name):
-    path = os.path.join(GOLDEN, f"{name}_q0.npz")
+@pytest.mark.parametrize("name,q", [("cfg1", 0), ("cfg2", 0), ("cfg2", 1), ("cfg2", 2), ("cfg3", 0), ("cfg3", 1),
+                                    ("cfg5", 0), ("cfg5", 1)])
+def test_config_fixture_fingerprint_and_p1(name, q):
+    path = os.path.join(GOLDEN, f"{name}_q{q}.npz")
     if not os.path.exists(path):
-        pytest.skip(f"{name} fixture not generated")
+        pytest.skip(f"{name} q{q} fixture not generated")
     import hashlib
 
     z = np.load(path)
-    case = W.gen_query(name, 0)
+    case = W.gen_query(name, q)
     h = hashlib.sha256()
     for a in (case.query, case.doc_tokens, case.doc_offsets):
         a = np.ascontiguousarray(a)
@@ -164,6 +165,22 @@ def test_config_fixture_fingerprint_and_p1(name):
         rtol = 1e-14 if name == "cfg1" else 0.0
         np.testing.assert_allclose(scores, z["scores"], rtol=rtol, atol=0)
         assert topk == z["topk"].tolist()
+
+
+@pytest.mark.parametrize("q", [1, 2])
+def test_cfg2_bandit_oracle_matches_reference(q):
+    """The oracle loop on more full-shape cfg2 queries (seed (0, q)) against the reference's traces."""
+    path = os.path.join(GOLDEN, f"cfg2_q{q}.npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture not generated")
+    z = np.load(path)
+    case = W.gen_query("cfg2", q)
+    cells = maxsim_ref.cell_matrix(case.query64(), case.docs64())
+    res = bandit_ref.run(cells, -1.0, 1.0, 10, seed=(0, q))
+    assert res.topk == z["a0_topk"].tolist()
+    np.testing.assert_array_equal(np.array([(i, t) for i, t, _ in res.reveals]), z["a0_trace_it"])
+    np.testing.assert_array_equal([v for *_, v in res.reveals], z["a0_trace_v"])
+    assert res.coverage == z["a0_stats"][0] and res.iterations == z["a0_stats"][1]
 
 
 def test_cfg1_bandit_oracle_matches_reference():

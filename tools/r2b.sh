@@ -1,0 +1,5 @@
+set -x
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/r2b_pytest.log 2>&1; echo "pytest rc=$?"
+tail -5 gpurun_out/r2b_pytest.log
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/r2b_bench.json 2> gpurun_out/r2b_bench.err; echo "bench rc=$?"
+tail -5 gpurun_out/r2b_bench.err
