@@ -304,6 +304,49 @@ CBX_API int cbx_bandit_shard_step(const cbx_batch* b, const double* matrix, int6
                                   int32_t* topk, int32_t max_k, int32_t* trace_i, int32_t* trace_t,
                                   double* trace_v, cbx_bandit_out* out, void* stream);
 
+/* Document-sharded Col-Bandit in ONE persistent launch per rank (the device-
+ * initiated exchange of SURVEY §5 / §7.2(4)): the same replicated-state
+ * protocol as cbx_bandit_shard_step, but the owner of a revealed cell stores
+ * its value straight into every other rank's inbox (slot = the cell's trace
+ * position: value, then a system-scope release store of the slot's flag) and
+ * the other ranks spin on an acquire load of their own inbox's flag — no
+ * kernel boundary, no host, no collective per iteration. The warm-up cells go
+ * the same way (one slot per warm-up cell).
+ * An inbox holds N*T slots (cbx_mbox_alloc: one cudaMalloc, so a CUDA IPC
+ * handle maps exactly it); its flags must be zero before the launch, and no
+ * rank may launch before every rank has zeroed its inbox. ``peers`` (device,
+ * [n_local][n_ranks]) gives, for each local rank, every rank's inbox as that
+ * rank's CTA addresses it (peer pointers from cbx_ipc_open across processes;
+ * plain device pointers when several ranks share one launch, n_local > 1,
+ * which is then a cooperative launch so that all of them are resident).
+ * runs[c] / own[2c], own[2c+1] (device) describe local rank rank0 + c: the
+ * same run (identical descriptor but trace_off/state_off) and its owned rows.
+ * Outputs as cbx_bandit_run, identical on every rank: the trace is reveal-for-
+ * reveal the single-GPU trace. */
+#define CBX_IPC_HANDLE_BYTES 64
+typedef struct cbx_mbox_peer {
+  double* val;      /* [N*T] cell values by trace position */
+  int32_t* flag;    /* [N*T] 1 = value present           */
+} cbx_mbox_peer;
+CBX_API int cbx_bandit_shard_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix,
+                                 const cbx_bandit_run_desc* runs, int32_t n_local, const int64_t* own,
+                                 int32_t rank0, int32_t n_ranks, const cbx_mbox_peer* peers, int32_t max_rows,
+                                 const double* bounds_lo, const double* bounds_hi, const int32_t* warm_cells,
+                                 void* state, size_t state_bytes, int32_t* topk, int32_t max_k,
+                                 int32_t* trace_i, int32_t* trace_t, double* trace_v, cbx_bandit_out* out,
+                                 void* stream);
+/* One inbox of `slots` slots in its own device allocation (*bytes = its size, for the zeroing memset). */
+CBX_API int cbx_mbox_alloc(int64_t slots, void** base, size_t* bytes);
+CBX_API int cbx_mbox_free(void* base);
+/* Zero an inbox's flags (stream-ordered) before a run. */
+CBX_API int cbx_mbox_clear(void* base, int64_t slots, void* stream);
+/* The (val, flag) view of an inbox allocation (or of a peer's mapping of it). */
+CBX_API int cbx_mbox_view(void* base, int64_t slots, cbx_mbox_peer* view);
+/* CUDA IPC of an inbox between the ranks' processes (NVLink peer mappings). */
+CBX_API int cbx_ipc_get_handle(void* base, void* handle64);
+CBX_API int cbx_ipc_open(const void* handle64, void** base);
+CBX_API int cbx_ipc_close(void* base);
+
 /* The loop's numpy Generator(PCG64) replica, exposed to pin it against numpy
  * streams (tests/golden/pcg64_streams.json): starting from *state (host
  * struct), draw j is Generator.random() (float64 bits in out[j]) when

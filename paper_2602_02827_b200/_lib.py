@@ -31,6 +31,11 @@ CBX_BANDIT_MAX_COLS = 128
 CBX_BANDIT_EDESC = 3
 CBX_BANDIT_STEP_BYTES = 256
 CBX_SHARD_REVEAL, CBX_SHARD_WARMUP, CBX_SHARD_DONE = 0, 1, 2
+CBX_IPC_HANDLE_BYTES = 64
+
+
+class CbxMboxPeer(ctypes.Structure):
+    _fields_ = [("val", ctypes.c_void_p), ("flag", ctypes.c_void_p)]
 
 
 class CbxBatch(ctypes.Structure):
@@ -123,6 +128,15 @@ SIGNATURES = {
     "cbx_bandit_state_bytes": (_SZ, [_I64]),
     "cbx_bandit_set_profile": (None, [_P]),
     "cbx_pcg64_draws": (_I, [_P, _P, _I64, _P, _P, _P]),
+    "cbx_bandit_shard_run": (_I, [_P, _P, _I64, _P, _I32, _P, _I32, _I32, _P, _I32, _P, _P, _P, _P, _SZ, _P, _I32, _P,
+                                  _P, _P, _P, _P]),
+    "cbx_mbox_alloc": (_I, [_I64, _P, _P]),
+    "cbx_mbox_free": (_I, [_P]),
+    "cbx_mbox_clear": (_I, [_P, _I64, _P]),
+    "cbx_mbox_view": (_I, [_P, _I64, _P]),
+    "cbx_ipc_get_handle": (_I, [_P, _P]),
+    "cbx_ipc_open": (_I, [_P, _P]),
+    "cbx_ipc_close": (_I, [_P]),
     "cbx_bandit_run": (_I, [_P, _P, _I64, _P, _I64, _I32, _P, _P, _P, _P, _SZ, _P, _I32, _P, _P, _P, _P, _P]),
     "cbx_bandit_prewarm": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P]),
     "cbx_bandit_shard_step": (_I, [_P, _P, _I64, _P, _I64, _I64, _I, _P, _P, _P, _P, _SZ, _P, _P, _P, _I32, _P, _P,

@@ -23,6 +23,8 @@
 // interval from precomputed sqrt tables) and the Top-K membership.
 // Ranking and per-row state live in shared memory when the pool fits,
 // otherwise in global memory.
+#include <cstring>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -133,6 +135,13 @@ struct BanditParams {
   int64_t own_lo, own_hi;   // rows whose tokens this rank holds
   int64_t* xchg;            // exchange slots, all-reduced with MAX between launches
   struct BdStep* step;
+  // document-sharded run in ONE persistent launch (cbx_bandit_shard_run): the owner of a cell stores its
+  // value into every peer's inbox (NVLink peer memory / this GPU's memory) and the others wait on their own
+  // inbox's flag — no parking, no host round trip. CTA c of the launch is rank mb_rank0 + c.
+  int mbox;
+  int mb_ranks, mb_rank0;
+  const cbx_mbox_peer* mb_peers;  // [grid][mb_ranks] inboxes of every rank, as seen by CTA c
+  const int64_t* mb_own;          // [grid][2] owned row range of CTA c
 };
 
 // Resumable loop state of a sharded run (lives in global memory between launches).
@@ -148,6 +157,20 @@ struct BdStep {
   int32_t warmed, pad;
 };
 static_assert(sizeof(BdStep) <= CBX_BANDIT_STEP_BYTES, "step state");
+
+// mailbox protocol: value store, then a release store of the flag (system scope: the inbox may be a peer
+// GPU's memory over NVLink); the reader spins on an acquire load of its own inbox's flag
+__device__ __forceinline__ void mbox_publish(const cbx_mbox_peer& to, int64_t slot, double v) {
+  to.val[slot] = v;
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(to.flag + slot), "r"(1u) : "memory");
+}
+__device__ __forceinline__ double mbox_wait(const cbx_mbox_peer& mine, int64_t slot) {
+  uint32_t f;
+  do {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(f) : "l"(mine.flag + slot) : "memory");
+  } while (f == 0u);
+  return *reinterpret_cast<volatile const double*>(mine.val + slot);
+}
 
 // cell value <-> exchange slot: signed order == value order, INT64_MIN = "not mine"
 __device__ __forceinline__ int64_t xchg_key(uint64_t ordkey) { return (int64_t)(ordkey ^ 0x8000000000000000ull); }
@@ -746,10 +769,15 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
       o.status = CBX_BANDIT_EDESC;
       o.pad = 0;
       P.out[blockIdx.x] = o;
-      if (P.shard) P.step->phase = CBX_SHARD_DONE;
+      if (P.shard && P.step) P.step->phase = CBX_SHARD_DONE;
     }
     return;
   }
+  // owned rows of this CTA's rank (sharded runs)
+  const int64_t own_lo = P.mbox ? P.mb_own[2 * blockIdx.x] : P.own_lo;
+  const int64_t own_hi = P.mbox ? P.mb_own[2 * blockIdx.x + 1] : P.own_hi;
+  const int my_rank = P.mbox ? P.mb_rank0 + (int)blockIdx.x : 0;
+  const cbx_mbox_peer* peers = P.mbox ? P.mb_peers + (size_t)blockIdx.x * P.mb_ranks : nullptr;
   // UNI: every run of the launch has uniform (generic) bounds, so the per-cell-bound code compiles away
   // (a smaller hot loop: measured 2-4 % faster on cfg2/3/5)
   const bool uniform = UNI || R.bounds_off < 0;
@@ -942,8 +970,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
 
   // ------------------------------------------------------------ initial state (all n = 0)
   BdStep* const step = P.step;
-  const bool resume = P.shard && !P.first;
-  if (P.shard && step->phase == CBX_SHARD_DONE) return;
+  const bool resume = P.shard && !P.mbox && !P.first;
+  if (P.shard && !P.mbox && step->phase == CBX_SHARD_DONE) return;
   if (tid == 0) {
     ctrl->status = resume ? step->status : 0;
     ctrl->n_reveals = resume ? step->n_reveals : 0;
@@ -1187,14 +1215,28 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
       // one warp per cell: every token of the row once, dotted with its query token (a shard: its rows only)
       for (int64_t s = warp; s < (pre ? 0 : m); s += BD_WARPS) {
         const int i = tr_i[base + s];
-        const bool own = !P.shard || (i >= P.own_lo && i < P.own_hi);
+        const bool own = !P.shard || (i >= own_lo && i < own_hi);
+        if (P.mbox && !own) continue;  // (warp-uniform) another rank computes and sends it
         const double v = own ? cell_warp(i, tr_t[base + s]) : 0.0;
         if (lane == 0) {
-          if (P.shard) P.xchg[s] = own ? xchg_key(ord_key(v)) : INT64_MIN;
-          else tr_v[base + s] = v;
+          if (P.mbox) {
+            tr_v[base + s] = v;
+            for (int p = 0; p < P.mb_ranks; ++p)
+              if (p != my_rank) mbox_publish(peers[p], base + s, v);
+          } else if (P.shard) {
+            P.xchg[s] = own ? xchg_key(ord_key(v)) : INT64_MIN;
+          } else {
+            tr_v[base + s] = v;
+          }
         }
       }
-      if (P.shard) {
+      if (P.mbox) {
+        // the cells of the other ranks' rows arrive in this rank's inbox
+        for (int64_t s = tid; s < m; s += BD_THREADS) {
+          const int i = tr_i[base + s];
+          if (i < own_lo || i >= own_hi) tr_v[base + s] = mbox_wait(peers[my_rank], base + s);
+        }
+      } else if (P.shard) {
         park(2, CBX_SHARD_WARMUP, base, m);
         return;
       }
@@ -1207,7 +1249,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
     // ---------------------------------------------------------- reveal one cell
     i_star = ctrl->i_star;
     t_star = ctrl->t_star;
-    const bool own = !P.shard || (i_star >= P.own_lo && i_star < P.own_hi);
+    const bool own = !P.shard || (i_star >= own_lo && i_star < own_hi);
     if (tokens && own) {
       double best = tokens_max<T, G, VPL, B>(dtok, dto[i_star], dto[i_star + 1], qtok + (int64_t)t_star * dim, dim,
                                              gid, NGROUPS, sub, init_cell, warp, BD_WARPS, &ctrl->cellkey);
@@ -1220,12 +1262,29 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
       __syncthreads();
     }
     if (__builtin_expect(P.shard, 0)) {
-      if (tid == 0) {
-        const double v = tokens ? ord_val(ctrl->cellkey) : P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
-        P.xchg[0] = own ? xchg_key(ord_key(v)) : INT64_MIN;
+      if (P.mbox) {
+        // the owner sends the cell to every other rank; the others wait for it in their inbox
+        if (tid == 0) {
+          const int64_t pos = ctrl->n_reveals;
+          double v;
+          if (own) {
+            v = tokens ? ord_val(ctrl->cellkey) : P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
+            for (int p = 0; p < P.mb_ranks; ++p)
+              if (p != my_rank) mbox_publish(peers[p], pos, v);
+          } else {
+            v = mbox_wait(peers[my_rank], pos);
+          }
+          ctrl->cellkey = ord_key(v);
+        }
+        __syncthreads();
+      } else {
+        if (tid == 0) {
+          const double v = tokens ? ord_val(ctrl->cellkey) : P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
+          P.xchg[0] = own ? xchg_key(ord_key(v)) : INT64_MIN;
+        }
+        park(1, CBX_SHARD_REVEAL, 0, 0);
+        return;
       }
-      park(1, CBX_SHARD_REVEAL, 0, 0);
-      return;
     }
     } else if (resume_kind == 2) {
       // -------------------------------------------------------- sharded: warm-up values from the exchange
@@ -1343,7 +1402,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
     o.status = ctrl->status;
     o.pad = 0;
     P.out[blockIdx.x] = o;
-    if (P.shard) {
+    if (P.shard && !P.mbox) {
       step->phase = CBX_SHARD_DONE;
       step->pending = 0;
     }
@@ -1483,6 +1542,15 @@ static int launch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, cud
     if (P.bounds_lo == nullptr) kern = wide ? bandit_kernel<T, G, VPL, 512, true> : bandit_kernel<T, G, VPL, 256, true>;
   }
   CBX_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (P.mbox && n_runs > 1) {
+    // ranks of one launch wait on each other's mailboxes: they must all be resident at once
+    BanditParams Pc = P;
+    void* args[] = {&Pc};
+    cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3((unsigned)n_runs),
+                                                dim3(wide ? 512 : 256), args, smem, st);
+    if (e != cudaSuccess) return fail(CBX_ECUDA, std::string("bandit_kernel cooperative launch: ") + cudaGetErrorString(e));
+    return CBX_OK;
+  }
   kern<<<(unsigned)n_runs, wide ? 512 : 256, smem, st>>>(P);
   CBX_LAUNCH_CHECK("bandit_kernel launch");
   return CBX_OK;
@@ -1506,6 +1574,10 @@ struct ShardArgs {
   int first;
   int64_t* xchg;
   void* step;
+  // mailbox mode (cbx_bandit_shard_run)
+  int mbox, ranks, rank0;
+  const cbx_mbox_peer* peers;
+  const int64_t* own;
 };
 static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_matrix, const cbx_bandit_run_desc* runs,
                          int64_t n_runs, int32_t max_rows, const double* bounds_lo, const double* bounds_hi,
@@ -1554,9 +1626,78 @@ int cbx_bandit_shard_step(const cbx_batch* b, const double* matrix, int64_t ld_m
     return fail(CBX_EINVAL, "bandit shard: NULL buffer");
   if (!b && !matrix) return fail(CBX_EINVAL, "bandit shard: need token embeddings or a cell matrix");
   if (own_lo < 0 || own_hi < own_lo) return fail(CBX_EINVAL, "bandit shard: bad owned row range");
-  ShardArgs sa{own_lo, own_hi, first, xchg, step_state};
+  ShardArgs sa{own_lo, own_hi, first, xchg, step_state, 0, 0, 0, nullptr, nullptr};
   return launch_params(b, matrix, ld_matrix, run, 1, 0x7FFFFFFF, bounds_lo, bounds_hi, warm_cells, state, state_bytes,
                        topk, max_k, trace_i, trace_t, trace_v, out, stream, &sa);
+}
+
+int cbx_bandit_shard_run(const cbx_batch* b, const double* matrix, int64_t ld_matrix, const cbx_bandit_run_desc* runs,
+                         int32_t n_local, const int64_t* own, int32_t rank0, int32_t n_ranks,
+                         const cbx_mbox_peer* peers, int32_t max_rows, const double* bounds_lo,
+                         const double* bounds_hi, const int32_t* warm_cells, void* state, size_t state_bytes,
+                         int32_t* topk, int32_t max_k, int32_t* trace_i, int32_t* trace_t, double* trace_v,
+                         cbx_bandit_out* out, void* stream) {
+  if (!runs || !out || !topk || !trace_i || !trace_t || !trace_v || !state || !own || !peers)
+    return fail(CBX_EINVAL, "bandit shard run: NULL buffer");
+  if (!b && !matrix) return fail(CBX_EINVAL, "bandit shard run: need token embeddings or a cell matrix");
+  if (n_local < 1 || n_ranks < 1 || rank0 < 0 || rank0 + n_local > n_ranks)
+    return fail(CBX_EINVAL, "bandit shard run: ranks rank0 .. rank0 + n_local - 1 must lie in [0, n_ranks)");
+  if (n_local > sm_count()) return fail(CBX_EINVAL, "bandit shard run: more local ranks than SMs");
+  if (max_rows <= 0) return fail(CBX_EINVAL, "bandit shard run: max_rows must be positive");
+  ShardArgs sa{0, 0, 1, nullptr, nullptr, 1, n_ranks, rank0, peers, own};
+  return launch_params(b, matrix, ld_matrix, runs, n_local, max_rows, bounds_lo, bounds_hi, warm_cells, state,
+                       state_bytes, topk, max_k, trace_i, trace_t, trace_v, out, stream, &sa);
+}
+
+int cbx_mbox_alloc(int64_t slots, void** base, size_t* bytes) {
+  if (slots < 1 || !base || !bytes) return fail(CBX_EINVAL, "mbox_alloc: bad arguments");
+  const size_t nb = align_up((size_t)slots * sizeof(double), 256) + align_up((size_t)slots * sizeof(int32_t), 256);
+  void* p = nullptr;
+  CBX_CUDA_CHECK(cudaMalloc(&p, nb));  // its own allocation, so a CUDA IPC handle maps exactly this inbox
+  *base = p;
+  *bytes = nb;
+  return CBX_OK;
+}
+
+int cbx_mbox_clear(void* base, int64_t slots, void* stream) {
+  if (!base || slots < 1) return fail(CBX_EINVAL, "mbox_clear: bad arguments");
+  uint8_t* flags = static_cast<uint8_t*>(base) + align_up((size_t)slots * sizeof(double), 256);
+  CBX_CUDA_CHECK(cudaMemsetAsync(flags, 0, (size_t)slots * sizeof(int32_t), static_cast<cudaStream_t>(stream)));
+  return CBX_OK;
+}
+
+int cbx_mbox_free(void* base) {
+  if (base) CBX_CUDA_CHECK(cudaFree(base));
+  return CBX_OK;
+}
+
+int cbx_mbox_view(void* base, int64_t slots, cbx_mbox_peer* view) {
+  if (!base || slots < 1 || !view) return fail(CBX_EINVAL, "mbox_view: bad arguments");
+  view->val = static_cast<double*>(base);
+  view->flag = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(base) + align_up((size_t)slots * sizeof(double), 256));
+  return CBX_OK;
+}
+
+int cbx_ipc_get_handle(void* base, void* handle64) {
+  if (!base || !handle64) return fail(CBX_EINVAL, "ipc_get_handle: bad arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == CBX_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  CBX_CUDA_CHECK(cudaIpcGetMemHandle(&h, base));
+  std::memcpy(handle64, &h, sizeof(h));
+  return CBX_OK;
+}
+
+int cbx_ipc_open(const void* handle64, void** base) {
+  if (!handle64 || !base) return fail(CBX_EINVAL, "ipc_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  CBX_CUDA_CHECK(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+  return CBX_OK;
+}
+
+int cbx_ipc_close(void* base) {
+  if (base) CBX_CUDA_CHECK(cudaIpcCloseMemHandle(base));
+  return CBX_OK;
 }
 
 int cbx_bandit_prewarm(const cbx_batch* b, const cbx_bandit_run_desc* runs, int64_t n_runs, const int64_t* warm_prefix,
@@ -1663,15 +1804,22 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
   P.own_hi = sa ? sa->own_hi : 0;
   P.xchg = sa ? sa->xchg : nullptr;
   P.step = sa ? static_cast<BdStep*>(sa->step) : nullptr;
+  P.mbox = sa ? sa->mbox : 0;
+  P.mb_ranks = sa ? sa->ranks : 0;
+  P.mb_rank0 = sa ? sa->rank0 : 0;
+  P.mb_peers = sa ? sa->peers : nullptr;
+  P.mb_own = sa ? sa->own : nullptr;
   // widest run of the launch (sizes the per-cell bounds staged in shared memory): the batch's longest query,
   // or the matrix width
   const int64_t max_t = std::min<int64_t>(BD_MAX_T, b ? std::max(b->max_lq, 1) : std::max<int64_t>(ld_matrix, 1));
   size_t smem = 128 + sizeof(Cand) * 4 * 16 + 2 * sizeof(double) * (BD_MAX_T + 1);  // reductions: up to 16 warps
   smem = align_up(smem, 16);
-  P.use_smem = (max_rows <= BD_SMEM_ROWS && !sa) ? 1 : 0;  // a sharded run resumes from global state
+  // a host-stepped sharded run resumes from global state; a mailbox run is one launch like any other
+  const bool resumable = sa && !sa->mbox;
+  P.use_smem = (max_rows <= BD_SMEM_ROWS && !resumable) ? 1 : 0;
   if (P.use_smem) smem += (size_t)(max_rows + BD_ROW_SLACK) * ROW_STRIDE + 64;
   P.trees_smem = 0;
-  if (!P.use_smem && !sa && CBX_BD_WIDE && n_runs <= sm_count()) {
+  if (!P.use_smem && !resumable && CBX_BD_WIDE && n_runs <= sm_count()) {
     // 4 trees x (8-byte key + 4-byte tie) per node; nodes = sum over 32-ary levels
     int64_t nn = 0, sz = ((int64_t)max_rows + 31) / 32;
     for (int l = 0; l < 8; ++l) {
@@ -1687,7 +1835,7 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
   }
   P.bounds_smem = 0;
   P.bounds_smem_off = 0;
-  if (!sa && CBX_BD_WIDE && n_runs <= sm_count() && max_rows <= BD_SMEM_ROWS) {
+  if (!resumable && CBX_BD_WIDE && n_runs <= sm_count() && max_rows <= BD_SMEM_ROWS) {
     // 3 expansions per row, plus lo/hi for up to max_t columns per row when per-cell bounds are given
     const size_t need = (size_t)max_rows * 3 * sizeof(ExpStore) +
                         (bounds_lo ? (size_t)max_rows * max_t * 2 * sizeof(double) : 0);

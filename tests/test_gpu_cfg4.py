@@ -133,3 +133,18 @@ def test_p2_sharded_one_rank_trace(cfg4):
     case, b, z = cfg4
     run = ShardedBanditRun(b, (0, case.n_docs), BanditConfig(k=W.CONFIGS["cfg4"].k, seed=(0, 0)))
     _assert_trace(drive(run, lambda x, n: None), z)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_p2_mailbox_sharded_trace(cfg4, world):
+    """The persistent document-sharded run (one launch, `world` rank CTAs exchanging every revealed cell
+    through device-memory inboxes) reproduces the reference trace on every rank."""
+    from paper_2602_02827_b200 import BanditConfig
+    from paper_2602_02827_b200.dist import balanced_ranges
+    from paper_2602_02827_b200.sharded import run_local_shards
+
+    case, b, z = cfg4
+    res = run_local_shards(b, balanced_ranges(case.doc_offsets, world),
+                           BanditConfig(k=W.CONFIGS["cfg4"].k, seed=(0, 0)))
+    for r in res:
+        _assert_trace(r, z)

@@ -128,3 +128,49 @@ def test_drive_with_a_one_rank_group_matches_single_gpu():
     (run,) = _shard_runs(case, docs, 1, cfg)
     res = drive(run, lambda xchg, n: None, check_every=16)
     assert res.reveals == single.reveals and res.topk == single.topk
+
+
+# ---------------------------------------------------------------- the persistent mailbox exchange
+def _full_batch(case, docs):
+    from paper_2602_02827_b200.batch import TokenBatch
+
+    return TokenBatch.from_host([case.query], [docs])
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_mailbox_ranks_in_one_launch_match_single_gpu(world):
+    """cbx_bandit_shard_run with `world` co-resident rank CTAs exchanging through device-memory inboxes:
+    every rank's trace equals the single-GPU kernel's and the oracle's."""
+    from paper_2602_02827_b200 import BanditConfig
+    from paper_2602_02827_b200.dist import balanced_ranges
+    from paper_2602_02827_b200.sharded import run_local_shards
+
+    case, docs = _pool(600)
+    cfg = BanditConfig(k=10, seed=(0, 0))
+    single = _single(case, docs, cfg)
+    cells = maxsim_ref.cell_matrix(case.query64(), case.docs64())
+    ref = bandit_ref.run(cells, -1.0, 1.0, 10, seed=(0, 0))
+    assert single.reveals == ref.reveals
+    res = run_local_shards(_full_batch(case, docs), balanced_ranges(case.doc_offsets, world), cfg)
+    assert len(res) == world
+    for r in res:
+        assert r.reveals == single.reveals and r.topk == single.topk
+        assert (r.iterations, r.terminated_by, r.coverage) == (single.iterations, single.terminated_by,
+                                                               single.coverage)
+
+
+@pytest.mark.parametrize("mode", ["static-warmup", "uniform-row"])
+def test_mailbox_other_explore_modes_and_per_cell_bounds(mode):
+    from paper_2602_02827_b200 import BanditConfig, CellBounds
+    from paper_2602_02827_b200.dist import balanced_ranges
+    from paper_2602_02827_b200.sharded import run_local_shards
+
+    case, docs = _pool(300, q=1)
+    cells = maxsim_ref.cell_matrix(case.query64(), case.docs64())
+    rng = np.random.default_rng(7)
+    bounds = CellBounds(cells - rng.uniform(0.0, 0.3, cells.shape), cells + rng.uniform(0.0, 0.3, cells.shape))
+    cfg = BanditConfig(k=5, seed=(0, 1), explore_mode=mode, gamma_init=0.05, alpha_ef=0.3)
+    for bnd in ((-1.0, 1.0), bounds):
+        single = _single(case, docs, cfg, bnd)
+        for r in run_local_shards(_full_batch(case, docs), balanced_ranges(case.doc_offsets, 3), cfg, bnd):
+            assert r.reveals == single.reveals and r.topk == single.topk
