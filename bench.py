@@ -371,6 +371,8 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_p1_sharded:
         section("p1_sharded", lambda: run_p1_sharded(args, rank, world))
         torch.cuda.empty_cache()
+    if not args.no_drop_in:
+        section("drop_in", lambda: run_drop_in(args, rank, world))
     if not args.no_stage1:
         section("stage1", lambda: run_stage1(args, rank, world))
     if not args.no_p2_sharded:
@@ -403,6 +405,22 @@ def run_p1_sharded(args, rank, world):
         s_all = maxsim_scores(b)
         single = topk(s_all, b.q_doc_off, K, N)[0].cpu().numpy().ravel().tolist()
         del s_all
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import maxsim_ref
+
+        lim = _blas_one_thread()
+        n_s = 5000
+        q64 = b.q_tokens.double().cpu().numpy()
+        toks = b.d_tokens[: int(do[n_s])].double().cpu().numpy()
+        t0 = time.perf_counter()
+        maxsim_ref.score_query(q64, [toks[do[i]:do[i + 1]] for i in range(n_s)], K)
+        cpu_s = time.perf_counter() - t0
+        del lim, toks
+        T_ = int(qo[1] - qo[0])
+        cpu = {"value": n_s * T_ / cpu_s, "unit": "cells/s", "cores": 1, "kind": "port",
+               "full_query_s_extrapolated": cpu_s * N / n_s,
+               "sample": f"oracle/maxsim_ref over the first {n_s} of the 100k documents ({cpu_s:.1f} s)"}
     lo, hi = balanced_ranges(do, world)[rank]
     local = (do[lo:hi + 1] - do[lo]).astype(np.int64)
     shard = b.d_tokens[int(do[lo]):int(do[hi])].clone()
@@ -454,14 +472,17 @@ def run_p1_sharded(args, rank, world):
                     "pairs per rank, device Top-K merge by (-score, id)",
             "ranks": world, "ms": ms, "cells_per_s": N * T / (ms / 1e3),
             "doc_tokens_rank0": int(local[-1]), "exchange_bytes_per_rank": K * 12,
-            "topk_equal_single_gpu": merged == single, "gpu_launches": 3 + (2 if world > 1 else 0)}
+            "topk_equal_single_gpu": merged == single, "cpu_baseline": cpu,
+            "gpu_launches": 3 + (2 if world > 1 else 0)}
 
 
 def run_p2_sharded(args, rank, world):
     """cfg4 (one query, 100k candidates) Col-Bandit with the documents split over the ranks: each rank holds
-    its shard's tokens, keeps the replicated run state and exchanges the revealed value every iteration
-    (sharded.drive: cbx_bandit_shard_step + NCCL all-reduce MAX, 64 iterations per CUDA graph). Rank 0 also
-    runs the single-GPU persistent kernel on the whole pool and checks the traces are identical."""
+    its shard's tokens and keeps the replicated run state; the revealed value crosses to the other ranks
+    every iteration. Two exchange paths: "mailbox" (sharded.run_mailbox: ONE persistent kernel per rank, the
+    owner stores the cell into the peers' inboxes over NVLink peer memory) and "host_stepped" (sharded.drive:
+    a step kernel + NCCL all-reduce MAX per iteration, 64 per CUDA graph). Rank 0 also runs the single-GPU
+    kernel on the whole pool and checks that every trace is identical."""
     import numpy as np
     import torch
 
@@ -469,7 +490,7 @@ def run_p2_sharded(args, rank, world):
     from paper_2602_02827_b200 import workloads as W
     from paper_2602_02827_b200.batch import TokenBatch
     from paper_2602_02827_b200.dist import balanced_ranges
-    from paper_2602_02827_b200.sharded import ShardedBanditRun, allreduce_exchange, drive
+    from paper_2602_02827_b200.sharded import ShardedBanditRun, allreduce_exchange, drive, run_mailbox
 
     cfg = W.CONFIGS["cfg4"]
     b, (qo, do, qd) = W.gen_batch_device(cfg, n_queries=1, seed=0)  # the same pool on every rank
@@ -490,33 +511,134 @@ def run_p2_sharded(args, rank, world):
         e1.record()
         torch.cuda.synchronize()
         single_ms = e0.elapsed_time(e1)
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            # the reference's loop on this exact pool: oracle/bandit_ref over the float64 cells (the device cell
+            # kernel's cells are bit-equal to the reference's, tests/test_gpu_cfg4.py), trace checked live
+            from oracle import bandit_ref
+            from paper_2602_02827_b200.batch import exact_cells
+
+            cells = exact_cells(b, with_scores=False)[0][:, :T].cpu().numpy()
+            t0 = time.perf_counter()
+            ref = bandit_ref.run(cells, -1.0, 1.0, cfg.k, seed=(0, 0))
+            cpu_s = time.perf_counter() - t0
+            cpu = {"loop_s": cpu_s, "revealed_cells_per_s": len(ref.reveals) / cpu_s, "cores": 1, "kind": "port",
+                   "sample": "the whole cfg4 run: oracle/bandit_ref loop over precomputed float64 cells (row "
+                             "computation excluded: that is P1, see p1_sharded.cpu_baseline)",
+                   "trace_equal_device": ref.reveals == single.reveals and ref.topk == single.topk}
+            del cells
     del b
-    exchange = allreduce_exchange() if world > 1 else (lambda x, n: None)
-    run = ShardedBanditRun(sb, (lo, hi), bc)
-    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    # ---- mailbox: one persistent launch per rank
     if world > 1:
-        torch.distributed.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    res = drive(run, exchange)
-    e1.record()
-    torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms = float(t.item())
+        tm = {}
+        res_m = run_mailbox(sb, (lo, hi), bc, timing=tm)
+        mb_ms, = _reduce([tm["ms"]])
+    else:
+        from paper_2602_02827_b200.sharded import run_local_shards
+
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res_m = run_local_shards(sb, [(lo, hi)], bc)[0]
+        e1.record()
+        torch.cuda.synchronize()
+        mb_ms = e0.elapsed_time(e1)
+    # ---- host-stepped: step kernel + collective per iteration
+    hs = None
+    if not args.no_p2_host_stepped:
+        exchange = allreduce_exchange() if world > 1 else (lambda x, n: None)
+        run = ShardedBanditRun(sb, (lo, hi), bc)
+        torch.cuda.synchronize()
+        _barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res_h = drive(run, exchange)
+        e1.record()
+        torch.cuda.synchronize()
+        hs_ms, = _reduce([e0.elapsed_time(e1)])
+        hs = (res_h, hs_ms, run.steps)
     if rank != 0:
         return None
-    return {"what": "Col-Bandit run() on one cfg4 query (100k docs, Lq=32, d=128, f16, K=100), documents sharded "
-                    f"over {world} rank(s) by token count; replicated run state, one 8-byte all-reduce MAX per "
-                    "iteration (sharded.drive, 64 iterations per CUDA graph)",
-            "ranks": world, "ms": ms, "iterations": res.iterations, "reveals": len(res.reveals),
-            "us_per_iteration": ms * 1e3 / res.iterations,
-            "revealed_cells_per_s": len(res.reveals) / (ms / 1e3),
-            "single_gpu_persistent_ms": single_ms,
-            "trace_equal_single_gpu": res.reveals == single.reveals and res.topk == single.topk,
-            "exchange": "none (1 rank)" if world == 1 else "NCCL all-reduce MAX, 8 B per iteration, NVLink",
-            "gpu_launches": run.steps}
+    lens = np.diff(do)
+    gather = int(lens[res_m.reveals.i.astype(np.int64)].sum()) * 128 * 2
+    hbm_peak, _, peak_kind = _peaks()
+    out = {"what": "Col-Bandit run() on one cfg4 query (100k docs, Lq=32, d=128, f16, K=100), documents sharded "
+                   f"over {world} rank(s) by token count; replicated run state; every revealed cell crosses to "
+                   "the other ranks",
+           "ranks": world, "iterations": res_m.iterations, "reveals": len(res_m.reveals),
+           "single_gpu_persistent_ms": single_ms, "single_gpu_us_per_iteration": single_ms * 1e3 / single.iterations,
+           "cpu_baseline": cpu,
+           "mailbox": {"ms": mb_ms, "us_per_iteration": mb_ms * 1e3 / res_m.iterations,
+                       "revealed_cells_per_s": len(res_m.reveals) / (mb_ms / 1e3),
+                       "gather_frac_of_hbm_per_gpu": gather / world / (mb_ms / 1e3) / 1e9 / hbm_peak,
+                       "trace_equal_single_gpu": res_m.reveals == single.reveals and res_m.topk == single.topk,
+                       "exchange": "none (1 rank)" if world == 1 else
+                       "owner stores (value, flag) into every peer's inbox over NVLink (CUDA IPC), release/acquire",
+                       "gpu_launches": 1}}
+    if hs is not None:
+        res_h, hs_ms, steps = hs
+        out["host_stepped"] = {"ms": hs_ms, "us_per_iteration": hs_ms * 1e3 / res_h.iterations,
+                               "trace_equal_single_gpu": res_h.reveals == single.reveals and res_h.topk == single.topk,
+                               "exchange": "none (1 rank)" if world == 1 else
+                               "NCCL all-reduce MAX, 8 B per iteration, NVLink",
+                               "gpu_launches": steps}
+    return out
+
+
+def run_drop_in(args, rank, world):
+    """The reference-facing names on cfg2 queries, host arrays in, Python results out, validation included:
+    ``MaxSimOracle(QueryTokens(q), [DocTokens(...) x 1000], Similarity("dot", -1, 1))`` (oracle.py:107-144),
+    ``.exact_topk(10)`` (oracle.py:229-235) and ``run(oracle, CellBounds.uniform(...), BanditConfig(k=10,
+    seed=(0, q)))`` (bandit.py:169) — per query, as a caller of the reference would use them — beside the
+    reference algorithm on the same query (oracle port, one core) and a parity check of both outputs."""
+    if rank != 0:
+        return None
+    import numpy as np
+
+    from oracle import bandit_ref, maxsim_ref
+    from paper_2602_02827_b200 import (BanditConfig, CellBounds, DocTokens, MaxSimOracle, QueryTokens, Similarity,
+                                       run)
+    from paper_2602_02827_b200 import workloads as W
+
+    cfg = W.CONFIGS["cfg2"]
+    n_q = 3
+    t_build = t_topk = t_run = t_cpu_p1 = t_cpu_p2 = 0.0
+    same = True
+    lim = _blas_one_thread()
+    for q in range(n_q + 1):  # query 0 warms up (untimed)
+        case = W.gen_query(cfg, q)
+        off = case.doc_offsets
+        raw = [case.doc_tokens[off[i]:off[i + 1]] for i in range(case.n_docs)]
+        t0 = time.perf_counter()
+        oracle = MaxSimOracle(QueryTokens(case.query), [DocTokens(f"d{i}", x) for i, x in enumerate(raw)],
+                              Similarity("dot", -1.0, 1.0))
+        t1 = time.perf_counter()
+        top = oracle.exact_topk(cfg.k)
+        t2 = time.perf_counter()
+        res = run(oracle, CellBounds.uniform(case.n_docs, 32, -1.0, 1.0), BanditConfig(k=cfg.k, seed=(0, q)))
+        t3 = time.perf_counter()
+        q64, d64 = case.query64(), case.docs64()
+        t4 = time.perf_counter()
+        ref_s, ref_top, cells = maxsim_ref.score_query(q64, d64, cfg.k)
+        t5 = time.perf_counter()
+        ref = bandit_ref.run(maxsim_ref.cell_matrix(q64, d64), -1.0, 1.0, cfg.k, seed=(0, q))
+        t6 = time.perf_counter()
+        same &= top == list(ref_top) and res.reveals == ref.reveals and res.topk == ref.topk
+        if q:
+            t_build += t1 - t0
+            t_topk += t2 - t1
+            t_run += t3 - t2
+            t_cpu_p1 += t5 - t4
+            t_cpu_p2 += t6 - t5
+    del lim
+    return {"what": "reference-facing API per cfg2 query (1000 fp16 docs from host numpy arrays): MaxSimOracle "
+                    "construction (validation, float64 view, H2D), exact_topk(10), run(oracle, generic bounds, "
+                    "BanditConfig(k=10, seed=(0, q))); beside the reference algorithm (oracle port, 1 core)",
+            "queries": n_q, "construct_ms": t_build * 1e3 / n_q, "exact_topk_ms": t_topk * 1e3 / n_q,
+            "run_ms": t_run * 1e3 / n_q,
+            "cpu_reference": {"exact_topk_ms": t_cpu_p1 * 1e3 / n_q, "run_ms": t_cpu_p2 * 1e3 / n_q, "cores": 1,
+                              "kind": "port"},
+            "outputs_equal_reference_algorithm": bool(same), "gpu_launches": 4}
 
 
 def run_stage1(args, rank, world):
@@ -713,10 +835,14 @@ def run_bandit(args, batch, host_off, cfg, rank, world, qa=0):
     del lim
     out["parity"] = {"queries_checked": n_chk, "trace_identical": bool(same), "coverage_abs_err_max": cov_err}
     if world == 1 and not args.no_cpu:
-        out["cpu_baseline"] = {"value": cpu_rev / cpu_s, "unit": "revealed cells/s", "cores": 1, "kind": "port",
-                               "queries_per_s": n_chk / cpu_s,
-                               "sample": f"{n_chk} {cfg.name} queries: oracle/maxsim_ref cells + oracle/bandit_ref run, "
-                                         f"{cpu_s:.1f} s"}
+        cores = os.cpu_count() or 1
+        bwall, bouts = cpu_pool(cfg.name, cores, _ref_bandit_task, reps=1)
+        out["cpu_baseline"] = {"value": sum(r for _, r in bouts) / bwall, "unit": "revealed cells/s", "cores": cores,
+                               "kind": "port", "queries_per_s": cores / bwall,
+                               "sample": f"{cores} {cfg.name} Col-Bandit runs, one per process on every host core "
+                                         f"(rows + oracle/bandit_ref loop), {bwall:.1f} s wall",
+                               "one_core": {"value": cpu_rev / cpu_s, "queries_per_s": n_chk / cpu_s,
+                                            "sample": f"{n_chk} of this batch's queries, {cpu_s:.1f} s"}}
     return out
 
 
@@ -735,6 +861,7 @@ def _ref_init(cfg_name, worker_seed):
 
 
 def _ref_task(_):
+    """P1 of one query through the reference algorithm (oracle port): float64 cells, fsum scores, lexsort."""
     from oracle import maxsim_ref
 
     q, docs, k = _REF_STATE["case"]
@@ -743,31 +870,57 @@ def _ref_task(_):
     return time.perf_counter() - t0, len(docs) * q.shape[0]
 
 
-def run_reference(args):
+def _ref_bandit_task(q_index):
+    """P2 of one query through the reference algorithm: the rows it touches (all of them: the warm-up reveals
+    every row, oracle.py:205-215) + the loop (bandit_ref restates bandit.py:169-350), seed (0, q)."""
+    from oracle import bandit_ref, maxsim_ref
+
+    q, docs, k = _REF_STATE["case"]
+    t0 = time.perf_counter()
+    cells = maxsim_ref.cell_matrix(q, docs)
+    res = bandit_ref.run(cells, -1.0, 1.0, k, seed=(0, q_index))
+    return time.perf_counter() - t0, len(res.reveals)
+
+
+def cpu_pool(cfg_name, workers, fn, reps=1):
+    """Run fn once per worker per rep in a fork pool whose workers hold one query of the config; returns
+    (wall seconds of the timed maps, summed per-task results)."""
     import concurrent.futures as cf
     import multiprocessing as mp
 
+    ctx = mp.get_context("fork")
+    with cf.ProcessPoolExecutor(workers, mp_context=ctx, initializer=_ref_init, initargs=(cfg_name, 0)) as ex:
+        list(ex.map(_noop, range(workers)))  # initialise every worker (untimed)
+        t0 = time.perf_counter()
+        out = []
+        for _ in range(reps):
+            out += list(ex.map(fn, range(workers)))
+        wall = time.perf_counter() - t0
+    return wall, out
+
+
+def _noop(_):
+    time.sleep(0.05)
+    return 0
+
+
+def run_reference(args):
     from paper_2602_02827_b200 import workloads as W
 
     cfg = W.CONFIGS[args.config]
     cores = os.cpu_count() or 1
     workers = max(1, min(cores, args.ref_workers or cores))
-    ctx = mp.get_context("fork")
     # each worker generates one query of the config once (untimed), then scores it once per step
-    with cf.ProcessPoolExecutor(workers, mp_context=ctx, initializer=_ref_init, initargs=(cfg.name, 0)) as ex:
-        for _ in range(args.warmup):
-            list(ex.map(_ref_task, range(workers)))
-        t0 = time.perf_counter()
-        cells = 0
-        for _ in range(args.steps):
-            for _, c in ex.map(_ref_task, range(workers)):
-                cells += c
-        wall = time.perf_counter() - t0
+    cpu_pool(cfg.name, workers, _ref_task, reps=args.warmup)
+    wall, outs = cpu_pool(cfg.name, workers, _ref_task, reps=args.steps)
+    cells = sum(c for _, c in outs)
     value = cells / wall
+    # the Col-Bandit loop on the same cores (one run per worker, bounded)
+    bwall, bouts = cpu_pool(cfg.name, workers, _ref_bandit_task, reps=1)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
         "data": "synthetic (numpy, BASELINE.json configs[1] recipe)",
         "config": {"workload": f"{cfg.name}: {cfg.n_docs} docs/query, Lq={cfg.lq[0]}, d={cfg.dim}, {cfg.dtype}, "
                                f"K={cfg.k}", "queries_per_step": workers},
@@ -775,6 +928,9 @@ def run_reference(args):
                          "sample": f"{workers} {cfg.name} queries per step, one per process (ProcessPoolExecutor, "
                                    f"BLAS 1 thread each; oracle/maxsim_ref)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "bandit": {"revealed_cells_per_s": sum(r for _, r in bouts) / bwall, "queries_per_s": workers / bwall,
+                   "cores": workers, "kind": "port",
+                   "sample": f"{workers} {cfg.name} Col-Bandit runs (rows + oracle/bandit_ref loop), one per process"},
     }), flush=True)
 
 
@@ -866,7 +1022,9 @@ def main():
     ap.add_argument("--no-bandit", action="store_true")
     ap.add_argument("--no-p1-sharded", action="store_true")
     ap.add_argument("--no-stage1", action="store_true")
+    ap.add_argument("--no-drop-in", action="store_true")
     ap.add_argument("--no-p2-sharded", action="store_true")
+    ap.add_argument("--no-p2-host-stepped", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="launcher/sharding/reduction only, no GPU (gloo)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

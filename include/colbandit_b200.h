@@ -99,6 +99,10 @@ typedef struct cbx_batch {
   int32_t max_lq;             /* max query tokens over the batch */
   int64_t max_q_docs;         /* max documents of one query       */
   int64_t max_q_doc_tokens;   /* max candidate tokens of one query */
+  float d_norm_max;           /* an upper bound on every document token's L2 norm (cbx_token_norm_max);
+                                 required (> 0) by the bandit entry points for f16/bf16 tokens, where it
+                                 bounds the fp32 screen of the float64 reveal; ignored elsewhere */
+  int32_t reserved;
 } cbx_batch;
 
 CBX_API int cbx_abi_version(void);

@@ -55,6 +55,8 @@ class CbxBatch(ctypes.Structure):
         ("max_lq", ctypes.c_int32),
         ("max_q_docs", ctypes.c_int64),
         ("max_q_doc_tokens", ctypes.c_int64),
+        ("d_norm_max", ctypes.c_float),
+        ("reserved", ctypes.c_int32),
     ]
 
 

@@ -419,6 +419,8 @@ def prepare_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, prewarm: b
     tr_t = torch.empty(max(tr_off, 1), dtype=torch.int32, device=dev)
     tr_v = torch.empty(max(tr_off, 1), dtype=torch.float64, device=dev)
     out_t = torch.empty(nl * ctypes.sizeof(_lib.CbxBanditOut), dtype=torch.uint8, device=dev)
+    if batch is not None:
+        batch.norm_max()  # the fp32 reveal screen's error bound (cbx_batch.d_norm_max), computed once per batch
     bstruct = batch.struct() if batch is not None else None
     ld = matrix.shape[1] if matrix is not None else 0
     wprefix = None
@@ -465,6 +467,19 @@ def run_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, return_traces:
     return collect(raw, jobs, p["results"], return_traces)
 
 
+_STAGE = {}
+
+
+def _pinned_stage(nbytes: int):
+    """A grow-only pinned host buffer for trace copies (allocating pinned memory per call costs milliseconds)."""
+    import torch
+
+    t = _STAGE.get("buf")
+    if t is None or t.numel() < nbytes:
+        t = _STAGE["buf"] = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+    return t
+
+
 def collect(raw, jobs, results=None, return_traces: bool = True):
     """Fetch a launch's device outputs and build RunResults (raises on device-side errors)."""
     if results is None:
@@ -482,10 +497,20 @@ def collect(raw, jobs, results=None, return_traces: bool = True):
         cum = np.zeros(len(live) + 1, np.int64)
         np.cumsum(nrev, out=cum[1:])
         dev = raw["tr_i"].device
-        if int(cum[-1]):
-            shift = torch.from_numpy(np.repeat(starts - cum[:-1], nrev)).to(dev, non_blocking=True)
-            pos = torch.arange(int(cum[-1]), dtype=torch.int64, device=dev) + shift
-            tr_i, tr_t, tr_v = (raw[k][pos].cpu().numpy() for k in ("tr_i", "tr_t", "tr_v"))
+        total = int(cum[-1])
+        if total:
+            # one device gather of the used slots, two D2H copies into pinned memory, one synchronisation
+            shift = torch.from_numpy(np.repeat(starts - cum[:-1], nrev)).pin_memory().to(dev, non_blocking=True)
+            pos = torch.arange(total, dtype=torch.int64, device=dev) + shift
+            blk = torch.empty((total, 4), dtype=torch.int32, device=dev)  # (i, t, v lo word, v hi word)
+            blk[:, 0] = raw["tr_i"][pos]
+            blk[:, 1] = raw["tr_t"][pos]
+            blk[:, 2:].view(torch.float64)[:, 0] = raw["tr_v"][pos]
+            stage = _pinned_stage(total * 16)[: total * 16].view(torch.int32).view(total, 4)
+            stage.copy_(blk, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            h = stage.numpy().copy()  # the results own their memory; the pinned stage is reused
+            tr_i, tr_t, tr_v = h[:, 0], h[:, 1], h[:, 2:].view(np.float64)[:, 0]
         else:
             tr_i, tr_t, tr_v = np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.float64)
     for slot, r in enumerate(live):

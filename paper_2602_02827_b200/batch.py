@@ -174,7 +174,26 @@ class TokenBatch:
         s.max_lq = self.max_lq
         s.max_q_docs = self.max_q_docs
         s.max_q_doc_tokens = self.max_q_doc_tokens
+        s.d_norm_max = getattr(self, "_norm_max", 0.0) or 0.0
         return s
+
+    def norm_max(self) -> float:
+        """Upper bound on every document token's L2 norm (one device pass, cached): the bandit's fp32
+        reveal screen bounds its rounding error with it (cbx_batch.d_norm_max)."""
+        v = getattr(self, "_norm_max", None)
+        if v is None:
+            import torch
+
+            out = torch.zeros(1, dtype=torch.float32, device=self.d_tokens.device)
+            if self.d_tokens.shape[0]:
+                _lib.check(_lib.load().cbx_token_norm_max(self.d_tokens.data_ptr(), int(self.d_tokens.shape[0]),
+                                                          self.dim, dtype_code(self.d_tokens.dtype), out.data_ptr(),
+                                                          _stream_ptr()), "token_norm_max")
+            v = float(out.item())
+            # an all-zero (or empty) token set still needs a positive bound for the C ABI
+            v = v if v > 0.0 else 1e-30
+            self._norm_max = v
+        return v
 
 
 def _stream_ptr():

@@ -1,0 +1,8 @@
+// K2 bandit kernels for float tokens (see bandit_impl.cuh): one translation unit per dtype so the
+// instantiations compile in parallel. Built with -fmad=false like every bandit*.cu unit.
+#include "bandit_impl.cuh"
+
+namespace cbx {
+template int dispatch_bandit<float>(const BanditParams&, int64_t, size_t, cudaStream_t, int);
+template int dispatch_warm<float>(const BanditParams&, int, const int64_t*, unsigned, cudaStream_t);
+}  // namespace cbx

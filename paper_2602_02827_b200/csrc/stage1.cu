@@ -197,7 +197,7 @@ constexpr int S1_EPI_WARP0 = 4;
 constexpr int S1_ACC = 4;
 constexpr int S1_TILE = 128;
 constexpr int S1_MAX_STAGES = 6;
-constexpr int S1_MAX_KP = 64;
+constexpr int S1_MAX_KP = 256;  // per-row sorted tops live in shared memory (4 B x 128 rows x k')
 constexpr int S1_FCAP = 2048;  // refined candidates per row
 constexpr int S1_MIN_TOKENS = 8192;
 
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(S1R_THREADS)
   const int64_t r = blockIdx.x;
   const int rb = (int)(r / 128), rl = (int)(r % 128);
   const int n = p.P * p.kp;
-  float* sv = reinterpret_cast<float*>(rf_smem);                  // [P * kp] (<= 9472)
+  float* sv = reinterpret_cast<float*>(rf_smem);                  // [P * kp] (<= 148 * 256)
   uint64_t* fkey = reinterpret_cast<uint64_t*>(rf_smem);          // reused after the threshold: [S1_FCAP]
   uint32_t* ftok = reinterpret_cast<uint32_t*>(fkey + S1_FCAP);   // [S1_FCAP]
   float* qs = reinterpret_cast<float*>(ftok + S1_FCAP);           // [dim]
@@ -621,9 +621,20 @@ struct TcPlan {
   size_t smem, o_eps, o_gthr, o_cnt, o_ent, o_topv, o_tmax, total;
 };
 
+// shared memory of the scan for k': query block + sorted tops + scratch + >= 2 stages of tiles (plan_tc)
+static bool tc_fits(int dim, int kp) {
+  const size_t kblocks = (size_t)(dim + 63) / 64;
+  const size_t fixed = 1024 + kblocks * 16384 + 4 * (size_t)kp * 128 + 4 * 32 * 128 + 8 * 32;
+  if (fixed >= 227 * 1024) return false;
+  const size_t budget = 227 * 1024 - fixed;
+  const size_t tile_n = budget / (kblocks * 16384) >= 3 ? 128 : 64;
+  return budget / (kblocks * tile_n * 128) >= 2;
+}
+
 static bool tc_eligible(const cbx_batch* b, int kp) {
   return (b->dtype == CBX_F16 || b->dtype == CBX_BF16) && b->dim % 8 == 0 && b->dim <= 256 && kp <= S1_MAX_KP &&
-         b->n_d_tokens >= S1_MIN_TOKENS && b->n_d_tokens < (int64_t(1) << 31) && b->n_q_tokens < (int64_t(1) << 24);
+         tc_fits(b->dim, kp) && b->n_d_tokens >= S1_MIN_TOKENS && b->n_d_tokens < (int64_t(1) << 31) &&
+         b->n_q_tokens < (int64_t(1) << 24);
 }
 
 static int plan_tc(const cbx_batch* b, int kp, TcPlan& t) {
@@ -652,7 +663,7 @@ static int plan_tc(const cbx_batch* b, int kp, TcPlan& t) {
   t.o_gthr = take(4 * (size_t)R);
   t.o_cnt = take(4 * (size_t)t.items * 128);
   // expected appends per list ~ kp * (1 + ln(tokens per item / kp)); overflow falls back to SIMT
-  t.cap = std::min(1024, std::max(256, 12 * kp));
+  t.cap = std::min(4096, std::max(256, 12 * kp));
   t.o_ent = take(8 * (size_t)t.items * 128 * t.cap);
   t.o_topv = take(4 * (size_t)t.items * 128 * kp);
   // pre-pass sample: ~16 tiles per SM, at most 4096 tiles and 16 MB of tile maxima

@@ -145,11 +145,23 @@ def stage1_topk(corpus, rows, k_prime: int, clamp_negative: bool, path: str = "a
     return tok.cpu().numpy(), val.cpu().numpy()
 
 
+def _tc_fits(dim: int, kk: int) -> bool:
+    """The tcgen05 scan's shared memory for k' (mirrors tc_fits in csrc/stage1.cu): query block, k' sorted
+    tops per row, scratch and at least two tile stages within 227 KB."""
+    kb = (dim + 63) // 64
+    fixed = 1024 + kb * 16384 + 4 * kk * 128 + 4 * 32 * 128 + 8 * 32
+    if fixed >= 227 * 1024:
+        return False
+    budget = 227 * 1024 - fixed
+    tile_n = 128 if budget // (kb * 16384) >= 3 else 64
+    return budget // (kb * tile_n * 128) >= 2
+
+
 def _tc_eligible(corpus, kk) -> bool:
     import torch
 
     return (corpus.tokens.dtype in (torch.float16, torch.bfloat16) and corpus.dim % 8 == 0 and corpus.dim <= 256
-            and kk <= 64 and corpus.n_tokens >= 8192)
+            and kk <= 256 and _tc_fits(corpus.dim, kk) and corpus.n_tokens >= 8192)
 
 
 @dataclass

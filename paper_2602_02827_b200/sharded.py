@@ -142,6 +142,7 @@ class ShardedBanditRun:
         self._tr_v = torch.empty(N * T, dtype=torch.float64, device=dev)
         self._out = torch.empty(ctypes.sizeof(_lib.CbxBanditOut), dtype=torch.uint8, device=dev)
         self._phase_host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+        batch.norm_max()
         self._bstruct = batch.struct()
         self._first = 1
         self.steps = 0
@@ -293,6 +294,7 @@ class MailboxRun:
         self._tr_t = torch.empty(self.n_local * N * T, dtype=torch.int32, device=dev)
         self._tr_v = torch.empty(self.n_local * N * T, dtype=torch.float64, device=dev)
         self._out = torch.empty(self.n_local * ctypes.sizeof(_lib.CbxBanditOut), dtype=torch.uint8, device=dev)
+        batch.norm_max()
         self._bstruct = batch.struct()
         self._peers = None
 

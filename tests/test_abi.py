@@ -35,7 +35,7 @@ def test_library_loads_and_exports_every_declared_symbol():
 
 def test_struct_layouts_match_the_header():
     # sizes follow the C layout (natural alignment, 64-bit)
-    assert ctypes.sizeof(_lib.CbxBatch) == 5 * 8 + 4 * 8 + 4 * 4 + 2 * 8
+    assert ctypes.sizeof(_lib.CbxBatch) == 5 * 8 + 4 * 8 + 4 * 4 + 2 * 8 + 4 + 4
     assert ctypes.sizeof(_lib.CbxPcg64) == 4 * 8 + 2 * 4
     assert ctypes.sizeof(_lib.CbxBanditOut) == 8 + 4 * 4
     assert ctypes.sizeof(_lib.CbxBanditRunDesc) == 152  # static_assert in csrc/bandit.cu

@@ -90,6 +90,10 @@ def test_generate_candidates_matches_reference_golden(path):
     ("f16", 96, 20_000, 7, 33, False, 0.3),       # dim not a multiple of 64, heavy duplication
     ("bf16", 64, 700_000, 40, 10, True, 0.01),    # large enough for the threshold pre-pass
     ("f16", 128, 900_000, 200, 5, False, 0.0),    # pre-pass with two row blocks
+    ("f16", 128, 60_000, 100, 128, False, 0.0),   # k' > 64: 128 sorted tops per row
+    ("bf16", 128, 800_000, 40, 128, True, 0.02),  # k' = 128 with the pre-pass
+    ("f16", 128, 120_000, 32, 256, False, 0.1),   # k' = 256 (64-row tiles)
+    ("bf16", 256, 60_000, 16, 100, True, 0.0),    # d = 256, k' = 100
 ])
 def test_tc_scan_equals_simt_scan(dt, d, n_tok, rows, kp, clamp, dup):
     from paper_2602_02827_b200.batch import Corpus
@@ -189,3 +193,30 @@ def test_reranker_errors():
     est = ColBanditReranker(similarity="dot").fit([np.ones((2, 8), np.float16)])
     with pytest.raises(ValueError, match="does not match corpus dim"):
         est.rerank(np.ones((2, 4), np.float16))
+
+
+def test_wide_query_and_large_k_prime_match_the_oracle():
+    """The facade with 100-token queries (the paper's multimodal queries reach 100 tokens) and k' = 128 on the
+    tcgen05 scan: candidates, ANN bounds and the reveal trace against the oracle restatement of
+    ColBanditReranker.rerank (oracle/stage1_ref.rerank, pinned to the reference goldens)."""
+    from oracle import stage1_ref
+    from paper_2602_02827_b200.pipeline import stage1_topk
+    from paper_2602_02827_b200.reranker import ColBanditReranker
+
+    rng = np.random.default_rng(100)
+    d, n_docs = 128, 120
+    lens = rng.integers(60, 160, n_docs)
+    toks = W._unit(rng.standard_normal((int(lens.sum()), d)))
+    off = np.concatenate([[0], np.cumsum(lens)])
+    stored = W._cast(toks, "f16")
+    docs = [stored[off[i]:off[i + 1]] for i in range(n_docs)]
+    est = ColBanditReranker(k=8, k_prime=128, similarity="dot", clamp_negative=True, random_state=3).fit(docs)
+    docs64 = [W.to_float64(x, "f16") for x in docs]
+    for qi in range(2):
+        q = W._cast(W._unit(rng.standard_normal((100, d))), "f16")
+        o = est.rerank(q, query_index=qi)
+        assert stage1_topk.last_paths == ["tc"]
+        top, ref, kept = stage1_ref.rerank(W.to_float64(q, "f16"), docs64, k=8, k_prime=128, clamp_negative=True,
+                                           random_state=3, query_index=qi)
+        assert list(o.candidates.doc_indices) == kept and list(o.doc_indices) == top
+        assert [tuple(x) for x in o.result.reveals] == [tuple(x) for x in ref.reveals]
