@@ -47,6 +47,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "MaxSim cells/sec (exhaustive rerank, oracle-matching Top-K)"
 UNIT = "cells/s"
+_T0 = time.perf_counter()
+
+
+def _log(msg: str) -> None:
+    """Progress to stderr (stdout carries the one JSON line): where the time goes, and where a stuck run stopped."""
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(f"bench [{time.perf_counter() - _T0:7.1f} s] {msg}", file=sys.stderr, flush=True)
 
 
 def _peaks():
@@ -215,6 +222,7 @@ def run_ours(args, rank, world, local_rank):
             ev[2].record(stream)
         return res
 
+    _log(f"batch of {nq} queries on rank {rank} generated; P1 timed region")
     # ------------------------------------------------ P1, device-resident inputs
     for _ in range(args.warmup):
         step()
@@ -262,6 +270,7 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": args.steps * 2,
         }
 
+    _log("P1 parity + 1-core CPU baseline")
     # ------------------------------------------------ P1 parity on sampled queries + CPU baseline
     if rank == 0:
         from oracle import maxsim_ref
@@ -297,6 +306,8 @@ def run_ours(args, rank, world, local_rank):
     # shuffled order), streams the candidates out of the corpus, scores, selects Top-K and reads it back.
     if not args.no_e2e:
         from paper_2602_02827_b200.batch import Corpus
+
+        _log("e2e through Corpus.rerank_topk")
 
         corpus = Corpus(batch.d_tokens, do)
         rng = np.random.default_rng(1234 + rank)
@@ -356,11 +367,19 @@ def run_ours(args, rank, world, local_rank):
     # a failure in one is recorded, not fatal (every rank runs the same code on the same shapes, so a
     # failure is symmetric across ranks)
     def section(name, fn):
+        elapsed, = _reduce([time.perf_counter() - _T0])  # max over ranks: the same decision everywhere
+        if elapsed >= args.budget_s:
+            _log(f"section {name}: skipped (past the --budget-s {args.budget_s:.0f} s time budget)")
+            if rank == 0:
+                result[name] = {"skipped": f"time budget of {args.budget_s:.0f} s used up by the earlier sections"}
+            return
+        _log(f"section {name}: start")
         try:
             out = fn()
         except Exception as e:  # noqa: BLE001
             out = {"error": f"{type(e).__name__}: {e}"[:500]}
             print(f"bench: section {name} failed: {out['error']}", file=sys.stderr, flush=True)
+        _log(f"section {name}: done")
         if rank == 0:
             result[name] = out
 
@@ -378,6 +397,7 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_p2_sharded:
         torch.cuda.empty_cache()
         section("bandit_sharded", lambda: run_p2_sharded(args, rank, world))
+    _log("done")
     if rank == 0:
         print(json.dumps(result), flush=True)
 
@@ -520,10 +540,11 @@ def run_p2_sharded(args, rank, world):
 
             cells = exact_cells(b, with_scores=False)[0][:, :T].cpu().numpy()
             t0 = time.perf_counter()
-            ref = bandit_ref.run(cells, -1.0, 1.0, cfg.k, seed=(0, 0))
+            ref = bandit_ref.run(cells, -1.0, 1.0, cfg.k, seed=(0, 0), indexed=True)
             cpu_s = time.perf_counter() - t0
             cpu = {"loop_s": cpu_s, "revealed_cells_per_s": len(ref.reveals) / cpu_s, "cores": 1, "kind": "port",
-                   "sample": "the whole cfg4 run: oracle/bandit_ref loop over precomputed float64 cells (row "
+                   "sample": "the whole cfg4 run: oracle/bandit_ref loop (indexed ranking: sorted key list + lazy heaps, "
+                             "as bandit.py:249-284) over precomputed float64 cells (row "
                              "computation excluded: that is P1, see p1_sharded.cpu_baseline)",
                    "trace_equal_device": ref.reveals == single.reveals and ref.topk == single.topk}
             del cells
@@ -836,6 +857,7 @@ def run_bandit(args, batch, host_off, cfg, rank, world, qa=0):
     out["parity"] = {"queries_checked": n_chk, "trace_identical": bool(same), "coverage_abs_err_max": cov_err}
     if world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
+        _log(f"bandit: CPU baseline on {cores} cores (spawned workers)")
         bwall, bouts = cpu_pool(cfg.name, cores, _ref_bandit_task, reps=1)
         out["cpu_baseline"] = {"value": sum(r for _, r in bouts) / bwall, "unit": "revealed cells/s", "cores": cores,
                                "kind": "port", "queries_per_s": cores / bwall,
@@ -882,20 +904,34 @@ def _ref_bandit_task(q_index):
     return time.perf_counter() - t0, len(res.reveals)
 
 
-def cpu_pool(cfg_name, workers, fn, reps=1):
-    """Run fn once per worker per rep in a fork pool whose workers hold one query of the config; returns
-    (wall seconds of the timed maps, summed per-task results)."""
+def cpu_pool(cfg_name, workers, fn, reps=1, timeout_s=240.0):
+    """Run fn once per worker per rep in a process pool whose workers hold one query of the config; returns
+    (wall seconds of the timed maps, summed per-task results). A process that has initialised CUDA must not
+    fork (the children inherit the driver's and OpenMP's locked state and can hang): it spawns fresh
+    interpreters instead; every map is bounded by ``timeout_s``."""
     import concurrent.futures as cf
     import multiprocessing as mp
 
-    ctx = mp.get_context("fork")
-    with cf.ProcessPoolExecutor(workers, mp_context=ctx, initializer=_ref_init, initargs=(cfg_name, 0)) as ex:
-        list(ex.map(_noop, range(workers)))  # initialise every worker (untimed)
+    cuda_up = False
+    if "torch" in sys.modules:
+        import torch
+
+        cuda_up = torch.cuda.is_initialized()
+    ctx = mp.get_context("spawn" if cuda_up else "fork")
+    ex = cf.ProcessPoolExecutor(workers, mp_context=ctx, initializer=_ref_init, initargs=(cfg_name, 0))
+    try:
+        list(ex.map(_noop, range(workers), timeout=timeout_s))  # initialise every worker (untimed)
         t0 = time.perf_counter()
         out = []
         for _ in range(reps):
-            out += list(ex.map(fn, range(workers)))
+            out += list(ex.map(fn, range(workers), timeout=timeout_s))
         wall = time.perf_counter() - t0
+    except BaseException:
+        for pr in list(getattr(ex, "_processes", {}).values()):  # a stuck worker must not outlive the bench
+            pr.kill()
+        ex.shutdown(wait=False, cancel_futures=True)
+        raise
+    ex.shutdown()
     return wall, out
 
 
@@ -1026,6 +1062,8 @@ def main():
     ap.add_argument("--no-p2-sharded", action="store_true")
     ap.add_argument("--no-p2-host-stepped", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="launcher/sharding/reduction only, no GPU (gloo)")
+    ap.add_argument("--budget-s", type=float, default=420.0,
+                    help="sections beside the headline start only while the run is younger than this (seconds)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.gpus < 1:

@@ -20,6 +20,13 @@ loop; it must agree with the reference reveal for reveal. Citations are to
 * result: Top-K of the final ranking, coverage = reveals / (N T) —
   bandit.py:349-350.
 
+``run(..., indexed=True)`` keeps the ranking in the reference's own kind of
+structures instead of re-sorting the pool every iteration — a sorted key list
+of (-proxy, i) whose first K entries are the Top-K, a winner heap of (lcb, i)
+and a loser heap of (-ucb, i) with lazy invalidation (bandit.py:249-284,
+329-347) — so a 100k-row pool (cfg4) costs O(log N) per iteration like the
+reference; both modes must produce the same result (tests/test_oracle_golden.py).
+
 The RNG is numpy's ``default_rng(seed)`` exactly as the reference uses it.
 Cells are supplied as the float64 N x T matrix the reference's oracle would
 return from ``row_values`` (see maxsim_ref.cell_matrix).
@@ -27,6 +34,7 @@ return from ``row_values`` (see maxsim_ref.cell_matrix).
 
 from __future__ import annotations
 
+import heapq
 import math
 from dataclasses import dataclass
 
@@ -76,7 +84,7 @@ def _pymax(a: float, b: float) -> float:
 
 def run(cells, lo, hi, k: int, *, delta: float = 0.01, alpha_ef: float = 1.0, epsilon: float = 0.1,
         explore_mode: str = "epsilon-greedy", gamma_init: float = 0.0, seed=0, c: float = 1.0,
-        union_mode: str = "per-document") -> RefResult:
+        union_mode: str = "per-document", indexed: bool = False) -> RefResult:
     cells = np.asarray(cells, dtype=np.float64)
     n_rows, n_cols = cells.shape
     lo = np.broadcast_to(np.asarray(lo, dtype=np.float64), cells.shape)
@@ -142,18 +150,85 @@ def run(cells, lo, hi, k: int, *, delta: float = 0.01, alpha_ef: float = 1.0, ep
     for i in range(n_rows):
         refresh(i)
     idx = np.arange(n_rows)
+
+    # ---- ranking structures of the indexed mode (bandit.py:249-284, 329-347)
+    keys = None          # SortedList of (-proxy, i): the first k entries are the Top-K
+    member = [False] * n_rows
+    ver = [0] * n_rows   # bumped whenever a row's interval changes: older heap entries are stale
+    win: list = []       # (lcb, i, ver) over members
+    lose: list = []      # (-ucb, i, ver) over the rest
+    key_of = [0.0] * n_rows
+
+    def push(i: int) -> None:
+        if member[i]:
+            heapq.heappush(win, (float(lcb[i]), i, ver[i]))
+        else:
+            heapq.heappush(lose, (-float(ucb[i]), i, ver[i]))
+
+    def rebuild() -> None:
+        nonlocal keys
+        from sortedcontainers import SortedList
+
+        for i in range(n_rows):
+            key_of[i] = -float(proxy[i]) + 0.0  # -0.0 ties with 0.0 (np.lexsort compares values)
+        keys = SortedList((key_of[i], i) for i in range(n_rows))
+        for i in range(n_rows):
+            member[i] = False
+        for _, i in keys[:k]:
+            member[i] = True
+        win.clear()
+        lose.clear()
+        for i in range(n_rows):
+            ver[i] += 1
+            push(i)
+
+    def moved(i: int) -> None:
+        """Row i was refreshed: re-rank it, swap Top-K membership across the boundary if it crossed."""
+        keys.remove((key_of[i], i))
+        key_of[i] = -float(proxy[i]) + 0.0
+        keys.add((key_of[i], i))
+        ver[i] += 1
+        pos_in = keys.index((key_of[i], i)) < k
+        if pos_in != member[i]:
+            member[i] = pos_in
+            # the row pushed across the boundary the other way: the new k-th entry, or the first of the rest
+            j = keys[k - 1][1] if not pos_in else keys[k][1]
+            member[j] = not pos_in
+            push(j)
+        push(i)
+
+    def boundary():
+        while True:
+            l, i, v = win[0]
+            if member[i] and v == ver[i]:
+                i_plus = i
+                break
+            heapq.heappop(win)
+        while lose:
+            u, i, v = lose[0]
+            if not member[i] and v == ver[i]:
+                return i_plus, i, -u
+            heapq.heappop(lose)
+        return i_plus, -1, -math.inf
+
+    if indexed:
+        rebuild()
     iterations = 0
     terminated_by = "separation"
+    order = None
     while True:
         iterations += 1
-        order = np.lexsort((idx, -proxy))
-        top, rest = order[:k], order[k:]
-        i_plus = int(top[np.lexsort((top, lcb[top]))[0]])
-        if len(rest):
-            i_minus = int(rest[np.lexsort((rest, -ucb[rest]))[0]])
-            ucb_minus = float(ucb[i_minus])
+        if indexed:
+            i_plus, i_minus, ucb_minus = boundary()
         else:
-            i_minus, ucb_minus = -1, -math.inf
+            order = np.lexsort((idx, -proxy))
+            top, rest = order[:k], order[k:]
+            i_plus = int(top[np.lexsort((top, lcb[top]))[0]])
+            if len(rest):
+                i_minus = int(rest[np.lexsort((rest, -ucb[rest]))[0]])
+                ucb_minus = float(ucb[i_minus])
+            else:
+                i_minus, ucb_minus = -1, -math.inf
         if lcb[i_plus] >= ucb_minus:
             break
         if not warmed:
@@ -169,6 +244,8 @@ def run(cells, lo, hi, k: int, *, delta: float = 0.01, alpha_ef: float = 1.0, ep
             if trace:
                 for i in range(n_rows):
                     refresh(i)
+                if indexed:
+                    rebuild()
             continue
         if len(trace) == n_rows * n_cols:
             terminated_by = "exhaustion"
@@ -192,7 +269,9 @@ def run(cells, lo, hi, k: int, *, delta: float = 0.01, alpha_ef: float = 1.0, ep
                     best, t_star = w, t
         reveal(i_star, t_star)
         refresh(i_star)
-    topk = [int(i) for i in order[:k]]
+        if indexed:
+            moved(i_star)
+    topk = [int(i) for _, i in keys[:k]] if indexed else [int(i) for i in order[:k]]
     return RefResult(topk, len(trace) / (n_rows * n_cols), trace, iterations, terminated_by)
 
 

@@ -719,6 +719,185 @@ __device__ __forceinline__ double tokens_max_screen(const T* __restrict__ dtok, 
   return best;
 }
 
+// 16-bit inputs with dim <= 256: the same interval screen with the fp32 dots taken by the
+// warp-level tensor-core MMA (mma.sync m16n8k16, fp32 accumulate) straight from registers — the reveal is a
+// latency-bound GEMV over one document, so operands staged through shared memory (TMA + tcgen05) would add a
+// barrier round trip per document, while the FMA screen above spends ~250 issue slots per 16 rows and warp;
+// this one spends ~25 (8 LDG.128 + 8 HMMA per 16 rows at d = 128).
+//  * A = 16 document tokens x 16 k per instruction. Lane (g = lane / 4, t = lane % 4) loads the 16-byte
+//    vector t of every 64-byte chunk of rows g and g + 8 (each warp load covers whole 32-byte sectors) and
+//    feeds its four words as the fragment's k positions {2t, 2t+1, 2t+8, 2t+9}: a dot product does not care
+//    about the order of k as long as B uses the same one, so B's fragment is the query's vector at the same
+//    byte offset. The query sits in every one of B's 8 columns: each lane reads its rows' sums off c0 / c2.
+//  * eps = dim 2^-19 xmax |q| + 2^-40 bounds the accumulation error of the tensor core's fp32 adder (exact
+//    16-bit products; the bound Stage 1 uses for tcgen05, validated there against the float64 scan).
+//  * LB is shared by the CTA's warps through an ordered-key atomicMax in shared memory (`shared_lb`) and a
+//    barrier before the exact pass, so only rows within 2 eps of the document's best fp32 dot — one or two
+//    per reveal — are recomputed in float64 (same fma order as the FMA screen's exact pass).
+template <typename T>
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  if constexpr (std::is_same<T, __half>::value)
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  else
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float ord_val_f(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+template <typename T, int KCMAX, int BT>
+__device__ __forceinline__ double tokens_max_mma(const T* __restrict__ dtok, int64_t j0, int64_t j1,
+                                                 const T* __restrict__ q, int dim, int wid, int nwarps, int lane,
+                                                 double best, unsigned int* shared_lb, float xmax) {
+  const int nvec = dim >> 3;        // 16-byte vectors per row
+  const int kc = (nvec + 3) >> 2;   // 64-byte chunks per row (the last one zero-padded when dim % 32 != 0)
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t ntile = (j1 - j0 + 15) >> 4;
+  const int64_t stride = (int64_t)nwarps * BT;
+  uint4 U[BT][KCMAX], V[BT][KCMAX];
+  // one step's loads: rows g and g + 8 of BT tiles (issued before anything that waits on data)
+  auto load_step = [&](int64_t tb) {
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+      const int64_t r0 = j0 + ((tb + (int64_t)b * nwarps) << 4) + g;
+      const uint4* p0 = reinterpret_cast<const uint4*>(dtok + r0 * dim) + t;
+      const uint4* p1 = reinterpret_cast<const uint4*>(dtok + (r0 + 8) * dim) + t;
+#pragma unroll
+      for (int c = 0; c < KCMAX; ++c) {
+        U[b][c] = make_uint4(0, 0, 0, 0);
+        V[b][c] = make_uint4(0, 0, 0, 0);
+        if (c * 4 + t < nvec && r0 < j1) U[b][c] = __ldg(p0 + c * 4);
+        if (c * 4 + t < nvec && r0 + 8 < j1) V[b][c] = __ldg(p1 + c * 4);
+      }
+    }
+  };
+  uint4 qv[KCMAX];
+#pragma unroll
+  for (int c = 0; c < KCMAX; ++c) {
+    qv[c] = make_uint4(0, 0, 0, 0);
+    if (c * 4 + t < nvec) qv[c] = __ldg(reinterpret_cast<const uint4*>(q) + c * 4 + t);
+  }
+  if (wid < ntile) load_step(wid);  // the document's first rows are in flight while |q| is taken
+  float nq2 = 0.0f;
+#pragma unroll
+  for (int c = 0; c < KCMAX; ++c) {
+    const T* x = reinterpret_cast<const T*>(&qv[c]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) nq2 = __fmaf_rn(Elem<T>::to_f(x[k]), Elem<T>::to_f(x[k]), nq2);
+  }
+  nq2 = __fadd_rn(nq2, __shfl_xor_sync(0xffffffffu, nq2, 1));
+  nq2 = __fadd_rn(nq2, __shfl_xor_sync(0xffffffffu, nq2, 2));
+  const bool screen = nq2 >= 0x1p-60f && nq2 <= 0x1p60f && xmax <= 0x1p60f;
+  const float qn = __fmul_ru(__fsqrt_ru(nq2), 1.0000005f);  // the fp32 |q|^2 above is within 2^-20 of the exact one
+  const float eps = __fmaf_ru(__fmul_ru(__fmul_ru(xmax, qn), (float)dim), 0x1p-19f, 0x1p-40f);
+  float LB = best == -INFINITY ? -INFINITY : __double2float_rd(best);
+  float p_ub = -INFINITY;  // pending list: entry `lane`
+  int64_t p_j = 0;
+  int pc = 0;
+
+  // exact float64 value of pending rows, highest ub first, until none can reach LB
+  auto flush = [&]() {
+    while (true) {
+      const uint32_t key = (lane < pc && !(p_ub < LB)) ? ord_key_f(p_ub) | 1u : 0u;  // NaN ub: ord_key_f > 0
+      const uint32_t kmax = __reduce_max_sync(0xffffffffu, key);
+      if (kmax == 0u) break;
+      const int L = __ffs(__ballot_sync(0xffffffffu, key == kmax)) - 1;
+      const int64_t j = __shfl_sync(0xffffffffu, p_j, L);
+      if (lane == L) p_ub = -INFINITY;
+      double acc = 0.0;
+      if (lane < nvec) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(dtok + j * dim) + lane);
+        const uint4 qw = __ldg(reinterpret_cast<const uint4*>(q) + lane);
+        const T* x = reinterpret_cast<const T*>(&w);
+        const T* y = reinterpret_cast<const T*>(&qw);
+        double part = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) part = fma(Elem<T>::to_d(x[k]), Elem<T>::to_d(y[k]), part);
+        acc += part;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (acc > best) {
+        best = acc;
+        LB = fmaxf(LB, __double2float_rd(acc));
+      }
+    }
+    pc = 0;
+  };
+
+  for (int64_t tb = wid; tb < ntile; tb += stride) {  // warp-uniform
+    float sv[BT][2];
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int c = 0; c < KCMAX; ++c) {
+        if (c < kc) {
+          mma16816<T>(acc, U[b][c].x, V[b][c].x, U[b][c].y, V[b][c].y, qv[c].x, qv[c].y);
+          mma16816<T>(acc, U[b][c].z, V[b][c].z, U[b][c].w, V[b][c].w, qv[c].z, qv[c].w);
+        }
+      }
+      sv[b][0] = acc[0];
+      sv[b][1] = acc[2];
+    }
+    if (tb + stride < ntile) load_step(tb + stride);  // the next step's rows fly during the bookkeeping below
+    float ub[BT][2];
+    float lbmax = -INFINITY;
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+      const int64_t r0 = j0 + ((tb + (int64_t)b * nwarps) << 4) + g;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float s = sv[b][h];
+        const bool live = r0 + 8 * h < j1;
+        ub[b][h] = !live ? -INFINITY : (screen ? __fadd_ru(s, eps) : INFINITY);
+        const float lb = __fsub_rd(s, eps);
+        if (live && screen && lb <= 3.0e38f && lb >= -3.0e38f) lbmax = fmaxf(lbmax, lb);  // finite only
+      }
+    }
+    // LB over the warp (and, through shared_lb, over the CTA's warps so far)
+    const uint32_t lk = __reduce_max_sync(0xffffffffu, lbmax == -INFINITY ? 0u : ord_key_f(lbmax));
+    if (lk) LB = fmaxf(LB, ord_val_f(lk));
+    if (shared_lb) {
+      if (lane == 0 && lk) atomicMax(shared_lb, lk);
+      const uint32_t sk = *reinterpret_cast<volatile unsigned int*>(shared_lb);
+      if (sk) LB = fmaxf(LB, ord_val_f(sk));
+    }
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        unsigned m = __ballot_sync(0xffffffffu, t == 0 && !(ub[b][h] < LB));
+        while (m) {  // warp-uniform: append the row of lane L to the pending list
+          const int L = __ffs(m) - 1;
+          m &= m - 1;
+          const float u = __shfl_sync(0xffffffffu, ub[b][h], L);
+          if (lane == pc) {
+            p_ub = u;
+            p_j = j0 + ((tb + (int64_t)b * nwarps) << 4) + (L >> 2) + 8 * h;
+          }
+          if (++pc == 32) flush();
+        }
+      }
+    }
+  }
+  if (shared_lb) {
+    // every warp has published its rows' lower bounds: the exact pass only sees the document's front-runners
+    __syncthreads();
+    const uint32_t sk = *reinterpret_cast<volatile unsigned int*>(shared_lb);
+    if (sk) LB = fmaxf(LB, ord_val_f(sk));
+  }
+  flush();
+  return best;
+}
+
+#ifndef CBX_BD_MMA
+#define CBX_BD_MMA 1  // tensor-core (mma.sync) screen for 16-bit tokens with dim <= 256
+#endif
 #ifndef CBX_BD_SCREEN
 #define CBX_BD_SCREEN 1
 #endif
@@ -731,8 +910,13 @@ __device__ __forceinline__ double tokens_max_screen(const T* __restrict__ dtok, 
 template <typename T, int G, int VPL, int B>
 __device__ __forceinline__ double tokens_max(const T* __restrict__ dtok, int64_t j0, int64_t j1, const T* q, int dim,
                                              int gid, int ngroups, int sub, double init, int wid, int nwarps,
-                                             const unsigned long long* shared_best, float xmax) {
+                                             const unsigned long long* shared_best, unsigned int* shared_lb, float xmax) {
   if constexpr (sizeof(T) == 2 && CBX_BD_SCREEN) {
+    if constexpr (CBX_BD_MMA && G * VPL <= 32) {
+      constexpr int KCMAX = (G * VPL) / 4;
+      return tokens_max_mma<T, KCMAX, (KCMAX <= 4 ? 2 : 1)>(dtok, j0, j1, q, dim, wid, nwarps, threadIdx.x & 31, init,
+                                                             shared_lb, xmax);
+    }
     constexpr int SG = (G * VPL) / 4 < 1 ? 1 : (G * VPL) / 4;
     return tokens_max_screen<T, SG, CBX_BD_SCREEN_B>(dtok, j0, j1, q, dim, wid, nwarps, threadIdx.x & 31, init,
                                                       shared_best, xmax);
@@ -804,7 +988,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
     int status;
     int64_t n_reveals;
     int iterations;
-    int pad;
+    unsigned int lbkey;         // CTA-wide fp32 lower bound of the cell being revealed (ordered key, 0 = none)
     unsigned long long cellkey;
     int32_t swap_in, swap_out;  // best non-member / worst member of the last selection
     int32_t partner;            // row whose membership swapped with i* this iteration (-1: none)
@@ -938,7 +1122,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
     if (!tokens) return P.matrix[(R.row_begin + i) * P.ld_matrix + t];
     double best = tokens_max<T, GW, VPL, (VPL == 1 ? 8 : 4)>(dtok, dto[i], dto[i + 1], qtok + (int64_t)t * dim,
                                                                    dim, lane / GW, 32 / GW, lane % GW, init_cell, 0, 1,
-                                                                   nullptr, P.xmax);
+                                                                   nullptr, nullptr, P.xmax);
 #pragma unroll
     for (int o = 16; o >= GW; o >>= 1) {
       const double w = __shfl_xor_sync(0xffffffffu, best, o);
@@ -1187,6 +1371,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
             ctrl->i_star = i_star;
             ctrl->t_star = t_star;
             ctrl->cellkey = ord_key(init_cell);
+            ctrl->lbkey = 0u;
 #if CBX_BD_DOC_PREFETCH
             if (tokens) {
               const int64_t j0 = i_star == i_plus ? jp0 : jm0, j1 = i_star == i_plus ? jp1 : jm1;
@@ -1300,7 +1485,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
       const int64_t j0 = dto[i_star], j1 = dto[i_star + 1];
 #endif
       double best = tokens_max<T, G, VPL, B>(dtok, j0, j1, qtok + (int64_t)t_star * dim, dim,
-                                             gid, NGROUPS, sub, init_cell, warp, BD_WARPS, &ctrl->cellkey, P.xmax);
+                                             gid, NGROUPS, sub, init_cell, warp, BD_WARPS, &ctrl->cellkey, &ctrl->lbkey,
+                                             P.xmax);
 #pragma unroll
       for (int o = 16; o >= G; o >>= 1) {
         const double w = __shfl_xor_sync(0xffffffffu, best, o);
@@ -1498,7 +1684,7 @@ __global__ void __launch_bounds__(256) warm_cells_kernel(const BanditParams P, i
     const int64_t* dto = P.d_tok_off + R.row_begin;
     const T* q = static_cast<const T*>(P.q_tokens) + (P.q_tok_off[R.query] + t) * (int64_t)P.dim;
     double best = tokens_max<T, GW, VPL, (VPL == 1 ? 8 : 4)>(dtok, dto[i], dto[i + 1], q, P.dim, lane / GW, 32 / GW,
-                                                             lane % GW, init_cell, 0, 1, nullptr, P.xmax);
+                                                             lane % GW, init_cell, 0, 1, nullptr, nullptr, P.xmax);
 #pragma unroll
     for (int o = 16; o >= GW; o >>= 1) {
       const double w = __shfl_xor_sync(0xffffffffu, best, o);

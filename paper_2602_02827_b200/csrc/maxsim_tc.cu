@@ -537,6 +537,291 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
+// ----------------------------------------------------------------- document-tile scorer (resident corpus)
+// The reranking service's scorer: the candidates of every query are scored in place in an HBM-resident
+// corpus (colbandit/oracle.py:205-227 for candidate lists). A tile is up to DT_ROWS consecutive rows of ONE
+// document, loaded where it lies by one TMA box per K block (box heights 8, 16, ..., DT_ROWS rows: at most
+// 7 rows of over-read per tile) and multiplied with N = ceil16(rows): no packed layout, no per-tile document
+// walk in the producer, no segment logic in the epilogue. Same roles and barriers as maxsim_tc_kernel;
+// a document longer than one tile hands its running max to the next tile through the carry chain.
+constexpr int DT_ROWS = 128;
+struct DocTmaps {
+  CUtensorMap d[DT_ROWS / 8];  // d[h - 1]: boxes of 8 h rows x 64 columns
+  CUtensorMap q;
+};
+
+// 32 documents of metadata per lane window, the next window loaded one window ahead
+struct DocWindow {
+  int64_t win, hi;
+  int64_t src, src_nx;
+  int32_t len, len_nx;
+  const int64_t* src_row;
+  const int32_t* doc_len;
+  bool want_src;
+  __device__ __forceinline__ void fetch(int64_t w, int lane, int64_t& s, int32_t& l) const {
+    s = 0;
+    l = 0;
+    if (w + lane < hi) {
+      l = __ldg(doc_len + w + lane);
+      if (want_src) s = __ldg(src_row + w + lane);
+    }
+  }
+  __device__ __forceinline__ void open(const TcParams& p, int64_t lo, int64_t hi_, int lane, bool with_src) {
+    src_row = p.src_row;
+    doc_len = p.doc_len;
+    want_src = with_src;
+    win = lo;
+    hi = hi_;
+    fetch(win, lane, src, len);
+    fetch(win + 32, lane, src_nx, len_nx);
+  }
+  // warp-collective: move the window so that it holds document d (documents are visited in order)
+  __device__ __forceinline__ void seek(int64_t d, int lane) {
+    while (d - win >= 32) {
+      win += 32;
+      src = src_nx;
+      len = len_nx;
+      fetch(win + 32, lane, src_nx, len_nx);
+    }
+  }
+  __device__ __forceinline__ int32_t length(int64_t d) const { return __shfl_sync(0xffffffffu, len, (int)(d - win)); }
+  __device__ __forceinline__ int64_t source(int64_t d) const { return __shfl_sync(0xffffffffu, src, (int)(d - win)); }
+};
+
+constexpr int DT_SLOTS = 16;  // tiles in flight (barrier pairs); their bytes share one ring
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    maxsim_docs_kernel(const __grid_constant__ DocTmaps tm, TcParams p) {
+  // Shared memory: the query operand, then ONE byte ring for the document tiles: a tile of h rows takes
+  // ceil8(h) x 128 B per K block, placed right behind its predecessor (wrapping to 0 when it would cross the
+  // end), so the ring holds ~40 % more bytes in flight than fixed 128-row stages do on ragged documents —
+  // the stream is latency bound, bytes in flight are bandwidth. Placement is a pure function of the tile
+  // sizes, so the MMA warp recomputes it; the producer alone tracks what has been consumed.
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* q_slot = smem;                                    // kblocks x (128 rows x 128 B)
+  uint8_t* ring = smem + p.q_slot_bytes;                     // ring_bytes (+ 1 KB the last tile's MMA may over-read)
+  const uint32_t C = (uint32_t)p.stages * p.stage_bytes;     // ring capacity (multiple of 1024)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + C + 1024);
+  uint64_t* full = bars;                                     // [DT_SLOTS]
+  uint64_t* empty = bars + DT_SLOTS;                         // [DT_SLOTS]
+  uint64_t* qfull = bars + 2 * DT_SLOTS;                     // [1]
+  uint64_t* qempty = qfull + 1;                              // [1]
+  uint64_t* tfull = qempty + 1;                              // [4]
+  uint64_t* tempty = tfull + TC_ACC_BUFS;                    // [4]
+  uint64_t* cfull = tempty + TC_ACC_BUFS;                    // [4] carry published
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cfull + TC_ACC_BUFS);
+  float* carry = reinterpret_cast<float*>(bars + 64);        // [4 slots][4 warps][32]
+  float* part = carry + 4 * 4 * 32;                          // [2 parity][4 quads]
+  uint64_t* vstart = reinterpret_cast<uint64_t*>(part + 8);  // [DT_SLOTS] virtual ring position of each tile in flight
+  static_assert(2 * DT_SLOTS + 2 + 3 * TC_ACC_BUFS + 1 <= 64, "barrier block");
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < DT_SLOTS; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(qfull, 1);
+    ptx::mbar_init(qempty, 1);
+    for (int s = 0; s < TC_ACC_BUFS; ++s) {
+      ptx::mbar_init(&tfull[s], 1);
+      ptx::mbar_init(&tempty[s], p.nq);
+      ptx::mbar_init(&cfull[s], p.nq);
+    }
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 0 && lane < DT_ROWS / 8) ptx::prefetch_tmap(&tm.d[lane]);
+  if (warp == 0 && lane == 31) ptx::prefetch_tmap(&tm.q);
+  if (warp == 1) ptx::tmem_alloc<TC_ACC_BUFS * TC_MAX_TILE_N>(tmem_holder);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (lane 0 issues)
+    uint32_t qphase = 0, tg = 0, tail = 0, off = 0;
+    uint64_t vpos = 0;
+    const uint64_t pol = ptx::policy_evict_first();
+    ChunkCursor cur;
+    cur.init(p);
+    ChunkInfo c;
+    while (cur.next(p, c)) {
+      if (lane == 0) {
+        ptx::mbar_wait(qempty, qphase ^ 1);
+        ptx::mbar_arrive_expect_tx(qfull, (uint32_t)(p.rep * p.kblocks * p.lqp * 128));
+        for (int g = 0; g < p.rep; ++g)
+          for (int kb = 0; kb < p.kblocks; ++kb)
+            ptx::tma_load_2d(q_slot + kb * 16384 + g * p.lqp * 128, &tm.q, qfull, kb * 64, (int32_t)c.q_tok0);
+      }
+      qphase ^= 1;
+      DocWindow w;
+      w.open(p, c.doc0, c.doc1, lane, true);
+      for (int64_t d = c.doc0; d < c.doc1; ++d) {
+        w.seek(d, lane);
+        const int32_t len = w.length(d);
+        const int64_t src = w.source(d);
+        if (lane == 0) {
+          for (int32_t r = 0; r < len; r += DT_ROWS, ++tg) {
+            const int h8 = ((len - r < DT_ROWS ? len - r : DT_ROWS) + 7) >> 3;  // box height / 8
+            const uint32_t kbytes = (uint32_t)h8 * 1024u, S = kbytes * (uint32_t)p.kblocks;
+            if (off + S > C) {  // the tile would cross the ring's end: it starts over at 0
+              vpos += C - off;
+              off = 0;
+            }
+            // tiles are consumed in order: wait for the oldest ones until none overlaps [vpos, vpos + S)
+            // (tile j overlaps iff its start is less than a ring length behind this tile's end)
+            while (tail < tg && (tg - tail == DT_SLOTS || vstart[tail % DT_SLOTS] + C < vpos + S)) {
+              ptx::mbar_wait(&empty[tail % DT_SLOTS], (tail / DT_SLOTS) & 1u);
+              ++tail;
+            }
+            const uint32_t slot = tg % DT_SLOTS;
+            vstart[slot] = vpos;
+            ptx::mbar_arrive_expect_tx(&full[slot], S);
+            for (int kb = 0; kb < p.kblocks; ++kb)
+              ptx::tma_load_2d_hint(ring + off + kb * kbytes, &tm.d[h8 - 1], &full[slot], kb * 64,
+                                    (int32_t)(src + r), pol);
+            off += S;
+            vpos += S;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (lane 0 issues)
+    uint32_t qphase = 0, tg = 0, off = 0;
+    ChunkCursor cur;
+    cur.init(p);
+    ChunkInfo c;
+    const uint32_t q_addr = ptx::smem_u32(q_slot);
+    const uint32_t ring_addr = ptx::smem_u32(ring);
+    const uint64_t ad0 = ptx::smem_desc_sw128(q_addr);
+    const uint32_t idesc0 = p.idesc & ~(0x3Fu << 17);  // N field cleared
+    while (cur.next(p, c)) {
+      if (lane == 0) {
+        ptx::mbar_wait(qfull, qphase);
+        ptx::tc_fence_after();
+      }
+      qphase ^= 1;
+      DocWindow w;
+      w.open(p, c.doc0, c.doc1, lane, false);
+      for (int64_t d = c.doc0; d < c.doc1; ++d) {
+        w.seek(d, lane);
+        const int32_t len = w.length(d);
+        if (lane == 0) {
+          for (int32_t r = 0; r < len; r += DT_ROWS, ++tg) {
+            const int32_t h = len - r < DT_ROWS ? len - r : DT_ROWS;
+            const uint32_t kbytes = (uint32_t)((h + 7) >> 3) * 1024u, S = kbytes * (uint32_t)p.kblocks;
+            if (off + S > C) off = 0;  // the producer's placement rule
+            const uint32_t idesc = idesc0 | ((uint32_t)(((h + 15) >> 4) * 2) << 17);
+            const uint32_t acc = tg & (TC_ACC_BUFS - 1), slot = tg % DT_SLOTS;
+            ptx::mbar_wait(&tempty[acc], ((tg >> 2) & 1) ^ 1);
+            ptx::mbar_wait(&full[slot], (tg / DT_SLOTS) & 1u);
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * TC_MAX_TILE_N;
+            const uint64_t bd0 = ptx::smem_desc_sw128(ring_addr + off);
+            const uint32_t bstep = kbytes >> 4;
+#pragma unroll
+            for (int kb = 0; kb < 8; ++kb) {
+              if (kb >= p.kblocks) break;
+#pragma unroll
+              for (int k4 = 0; k4 < 4; ++k4)
+                ptx::tc_mma_f16(d_tmem, ad0 + (uint64_t)(kb * 1024 + k4 * 2), bd0 + (uint64_t)(kb * bstep + k4 * 2),
+                                idesc, (kb | k4) != 0);
+            }
+            ptx::tc_commit(&empty[slot]);
+            ptx::tc_commit(&tfull[acc]);
+            off += S;
+          }
+        }
+      }
+      if (lane == 0) ptx::tc_commit(qempty);
+    }
+  } else if (warp >= TC_EPI_WARP0) {
+    // ------------------------------------------------------------ epilogue
+    // group g (nq warps, one per 32 query tokens) takes the tiles with index % rep == g; the lane of query
+    // token t keeps the max over the tile's columns, merges the carry of the document's earlier tiles and,
+    // on the document's last tile, the group sums over the query tokens.
+    const int quad = warp - TC_EPI_WARP0;
+    const int nq = p.nq, rep = p.rep;
+    const int grp = quad / nq, wig = quad - grp * nq;
+    if (grp < rep) {
+      const float init = p.clamp_negative ? 0.0f : -INFINITY;
+      const uint32_t tmem_lane = (uint32_t)(quad * 32) << 16;
+      uint32_t tg = 0, pb = 0;
+      ChunkCursor cursor;
+      cursor.init(p);
+      ChunkInfo c;
+      while (cursor.next(p, c)) {
+        const bool lane_valid = wig * 32 + lane < c.lq;
+        DocWindow w;
+        w.open(p, c.doc0, c.doc1, lane, false);
+        for (int64_t d = c.doc0; d < c.doc1; ++d) {
+          w.seek(d, lane);
+          const int32_t len = w.length(d);
+          for (int32_t r = 0; r < len; r += DT_ROWS, ++tg) {
+            if ((int)(tg % (uint32_t)rep) != grp) continue;
+            const int ncols = len - r < DT_ROWS ? len - r : DT_ROWS;
+            const uint32_t acc = tg & (TC_ACC_BUFS - 1);
+            ptx::mbar_wait(&tfull[acc], (tg >> 2) & 1);
+            ptx::tc_fence_after();
+            float v[DT_ROWS / 32][32];
+            const uint32_t taddr = tmem_base + tmem_lane + acc * TC_MAX_TILE_N;
+#pragma unroll
+            for (int b = 0; b < DT_ROWS / 32; ++b)
+              if (b * 32 < ncols) ptx::tmem_ld_32x32b_x32(taddr + b * 32, v[b]);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            float cur = init;
+#pragma unroll
+            for (int b = 0; b < DT_ROWS / 32; ++b) {
+              if (b * 32 >= ncols) break;
+              if (ncols - b * 32 >= 32) cur = fmaxf(cur, max32(v[b]));
+              else cur = masked_max(v[b], 0, ncols - b * 32, cur);
+            }
+            // carry chain (every tile waits for its predecessor's publication: keeps slot reuse ordered)
+            float p_prev = init;
+            if (tg > 0) {
+              const uint32_t ps = (tg - 1) & 3;
+              ptx::mbar_wait(&cfull[ps], ((tg - 1) >> 2) & 1);
+              p_prev = carry[(ps * 4 + wig) * 32 + lane];
+            }
+            if (r > 0) cur = fmaxf(cur, p_prev);
+            carry[((tg & 3) * 4 + wig) * 32 + lane] = cur;
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&cfull[tg & 3]);
+            if (r + DT_ROWS >= len) {  // the document's last tile
+              const float x = warp_sum(lane_valid ? cur : 0.0f);
+              if (nq == 1) {
+                if (lane == 0) p.scores[d] = x;
+              } else {
+                if (lane == 0) part[pb * 4 + quad] = x;
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(nq * 32) : "memory");
+                if (wig == 0 && lane == 0) {
+                  float sacc = part[pb * 4 + grp * nq];
+                  for (int k = 1; k < nq; ++k) sacc += part[pb * 4 + grp * nq + k];
+                  p.scores[d] = sacc;
+                }
+                pb ^= 1;
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<TC_ACC_BUFS * TC_MAX_TILE_N>(tmem_base);
+  }
+}
+
 // ----------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -630,7 +915,7 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t x, int64_t* wsum, int
 __global__ void __launch_bounds__(PL_THREADS)
     plan_local_kernel(const int64_t* __restrict__ corpus_off, int64_t n_corpus, const int64_t* __restrict__ cand,
                       int64_t n, int64_t* __restrict__ pk, int64_t* __restrict__ src_row, int32_t* __restrict__ len,
-                      int64_t* __restrict__ block_tot, int* __restrict__ status) {
+                      int64_t* __restrict__ block_tot, int* __restrict__ status, int64_t pack) {
   __shared__ int64_t wsum[PL_THREADS / 32];
   const int64_t j0 = (int64_t)blockIdx.x * PL_CHUNK + (int64_t)threadIdx.x * PL_PER;
   int64_t l8[PL_PER], t = 0;
@@ -648,7 +933,7 @@ __global__ void __launch_bounds__(PL_THREADS)
       }
       src_row[j] = s0;
       len[j] = (int32_t)L;
-      l8[u] = (L + TC_PACK - 1) & ~int64_t(TC_PACK - 1);
+      l8[u] = (L + pack - 1) & ~(pack - 1);
     }
     t += l8[u];
   }
@@ -773,12 +1058,17 @@ int launch_maxsim_tc(const cbx_batch* b, float* scores, cudaStream_t stream) {
 
 // Candidates of an HBM-resident corpus scored in place: b->d_tokens / n_d_tokens describe the corpus,
 // b->q_doc_off the per-query candidate ranges of cand_ids; no copy of the candidates is made.
+#ifndef CBX_PK_DOCS
+#define CBX_PK_DOCS 1  // resident-corpus scoring through maxsim_docs_kernel (0: the packed tile stream, A/B knob)
+#endif
 int launch_maxsim_tc_packed(const cbx_batch* b, const int64_t* corpus_off, int64_t n_corpus,
                             const int64_t* cand_ids, float* scores, void* ws, size_t ws_bytes, int* status,
                             cudaStream_t stream) {
   if (!tc_supported(b)) return fail(CBX_EINVAL, "tcgen05 scorer needs f16/bf16 tokens, Lq <= 128, dim % 8 == 0");
   const int64_t n = b->n_docs;
   if (n == 0 || b->n_queries == 0) return CBX_OK;
+  // document tiles of 128 rows need the K blocks of one stage to fit the ring (d <= 256)
+  const bool docs = CBX_PK_DOCS && b->dim <= 256;
   if (ws_bytes < packed_plan_bytes(n)) return fail(CBX_EINVAL, "packed scorer: workspace too small");
   uint8_t* w = static_cast<uint8_t*>(ws);
   int64_t* pk = reinterpret_cast<int64_t*>(w);
@@ -790,16 +1080,43 @@ int launch_maxsim_tc_packed(const cbx_batch* b, const int64_t* corpus_off, int64
   int64_t* btot = reinterpret_cast<int64_t*>(w);
   const int64_t nb = (n + PL_CHUNK - 1) / PL_CHUNK;
   plan_local_kernel<<<(unsigned)nb, PL_THREADS, 0, stream>>>(corpus_off, n_corpus, cand_ids, n, pk, src, len, btot,
-                                                             status);
+                                                             status, docs ? 8 : TC_PACK);
   CBX_LAUNCH_CHECK("plan_local_kernel launch");
   plan_blocks_kernel<<<1, PL_THREADS, 0, stream>>>(btot, nb);
   CBX_LAUNCH_CHECK("plan_blocks_kernel launch");
   plan_add_kernel<<<(unsigned)nb, PL_THREADS, 0, stream>>>(pk, n, btot, nb);
   CBX_LAUNCH_CHECK("plan_add_kernel launch");
   TcLaunch L;
-  int rc = prepare_tc(b, b->d_tokens, b->n_d_tokens, scores, L, CBX_PK_TILE_N);
+  int rc = prepare_tc(b, b->d_tokens, b->n_d_tokens, scores, L, docs ? DT_ROWS : CBX_PK_TILE_N);
   if (rc) return rc;
   L.p.packed = 1;
+  if (docs) {
+    // one tile = up to DT_ROWS rows of one document; CTAs own balanced ranges of the ceil8(len) prefix
+    static_assert(DT_ROWS == 128, "stage layout and TMEM buffers are sized for 128-row tiles");
+    DocTmaps tm;
+    for (int h = 1; h <= DT_ROWS / 8; ++h) {
+      rc = make_tmap(&tm.d[h - 1], b->d_tokens, b->dtype, b->n_d_tokens, b->dim, (uint32_t)(8 * h));
+      if (rc) return rc;
+    }
+    tm.q = L.tm.q;
+    {
+      // one byte ring instead of fixed stages: everything the barrier block and the query operand leave
+      const size_t bar_bytes = 512 + (4 * 4 * 32 + 8) * sizeof(float) + DT_SLOTS * sizeof(uint64_t);
+      const size_t ring = (227 * 1024 - 1024 /*align slack*/ - bar_bytes - L.p.q_slot_bytes - 1024 /*over-read*/) &
+                          ~size_t(1023);
+      L.p.stages = 1;
+      L.p.stage_bytes = (uint32_t)ring;
+      L.smem = 1024 + (size_t)L.p.q_slot_bytes + ring + 1024 + bar_bytes;
+    }
+    L.p.d_tok_off = pk;
+    L.p.src_row = src;
+    L.p.doc_len = len;
+    L.p.n_tokens_dev = pk + n;
+    CBX_CUDA_CHECK(cudaFuncSetAttribute(maxsim_docs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
+    maxsim_docs_kernel<<<L.grid, TC_THREADS, L.smem, stream>>>(tm, L.p);
+    CBX_LAUNCH_CHECK("maxsim_docs_kernel launch");
+    return CBX_OK;
+  }
   if (b->dim % 64 == 0) {
     for (int k = 0; k < 3; ++k) {
       const int h = L.p.tile_n >> k;

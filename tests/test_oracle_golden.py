@@ -73,7 +73,7 @@ def test_exact_topk_rejects_bad_k_and_breaks_ties_low():
 
 
 # ---------------------------------------------------------------- P2
-def _run_case(case):
+def _run_case(case, indexed=False):
     cfg = dict(case["cfg"])
     cfg["seed"] = _seed(cfg["seed"])
     k = cfg.pop("k")
@@ -82,12 +82,14 @@ def _run_case(case):
         lo, hi = np.array(case["lo"]), np.array(case["hi"])
     else:
         lo, hi = case["lo"], case["hi"]
-    return bandit_ref.run(cells, lo, hi, k, **cfg)
+    return bandit_ref.run(cells, lo, hi, k, indexed=indexed, **cfg)
 
 
-def test_bandit_oracle_matches_reference_trace_for_trace():
+@pytest.mark.parametrize("indexed", [False, True])
+def test_bandit_oracle_matches_reference_trace_for_trace(indexed):
+    # indexed: the sorted-key-list + lazy-heap ranking (the reference's structures) instead of a full sort
     for case in _load_json("p2_small.json"):
-        res = _run_case(case)
+        res = _run_case(case, indexed)
         exp = case["result"]
         assert [list(r) for r in res.reveals] == exp["reveals"]
         assert res.topk == exp["topk"]
