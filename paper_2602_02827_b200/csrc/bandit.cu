@@ -241,6 +241,7 @@ int cbx_bandit_prewarm(const cbx_batch* b, const cbx_bandit_run_desc* runs, int6
   P.dim = b->dim;
   P.clamp_negative = b->clamp_negative;
   P.xmax = b->d_norm_max;
+  P.mean_doc_rows = b->n_docs > 0 ? (int)std::min<int64_t>(b->n_d_tokens / b->n_docs, 1 << 30) : 0;
   if ((b->dtype == CBX_F16 || b->dtype == CBX_BF16) && !(b->d_norm_max > 0.0f))
     return fail(CBX_EINVAL, "bandit: 16-bit tokens need cbx_batch.d_norm_max > 0 (cbx_token_norm_max)");
   P.runs = runs;
@@ -293,6 +294,7 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
   P.matrix = matrix;
   P.ld_matrix = ld_matrix;
   P.xmax = b ? b->d_norm_max : 0.0f;
+  P.mean_doc_rows = b && b->n_docs > 0 ? (int)std::min<int64_t>(b->n_d_tokens / b->n_docs, 1 << 30) : 0;
   P.runs = runs;
   P.bounds_lo = bounds_lo;
   P.bounds_hi = bounds_hi;

@@ -113,6 +113,7 @@ struct BanditParams {
   const double* matrix;
   int64_t ld_matrix;
   float xmax;          // cbx_batch.d_norm_max: bound on the document tokens' norms (16-bit screen)
+  int mean_doc_rows;   // n_d_tokens / n_docs of the batch (picks the wide launch shape)
   const cbx_bandit_run_desc* runs;
   const double* bounds_lo;
   const double* bounds_hi;
@@ -733,7 +734,8 @@ __device__ __forceinline__ double tokens_max_screen(const T* __restrict__ dtok, 
 //    16-bit products; the bound Stage 1 uses for tcgen05, validated there against the float64 scan).
 //  * LB is shared by the CTA's warps through an ordered-key atomicMax in shared memory (`shared_lb`) and a
 //    barrier before the exact pass, so only rows within 2 eps of the document's best fp32 dot — one or two
-//    per reveal — are recomputed in float64 (same fma order as the FMA screen's exact pass).
+//    per reveal — are recomputed in float64, straight from the registers that still hold them (no second
+//    load) and in the fma / summation order of the FMA screen's exact pass (row_dot_exact), bit for bit.
 template <typename T>
 __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
@@ -749,8 +751,13 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
 __device__ __forceinline__ float ord_val_f(uint32_t k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
 }
+// Variant A (default, CBX_BD_MMA_REGS = 0): rows that survive the screen wait in a per-warp list and are
+// re-read (L1 / L2 hits) for the exact pass — the 64 staging registers are dead once the MMAs have consumed
+// them. Variant B (CBX_BD_MMA_REGS = 1, tokens_max_mma below) takes the exact dots from the staging registers
+// themselves; inside this kernel it spills (ptxas: 600 B of stack at the 128-register cap the two-CTA-per-SM
+// occupancy imposes) and measured 2x slower, so it is kept as a build knob only.
 template <typename T, int KCMAX, int BT>
-__device__ __forceinline__ double tokens_max_mma(const T* __restrict__ dtok, int64_t j0, int64_t j1,
+__device__ __forceinline__ double tokens_max_mma_reload(const T* __restrict__ dtok, int64_t j0, int64_t j1,
                                                  const T* __restrict__ q, int dim, int wid, int nwarps, int lane,
                                                  double best, unsigned int* shared_lb, float xmax) {
   const int nvec = dim >> 3;        // 16-byte vectors per row
@@ -781,7 +788,6 @@ __device__ __forceinline__ double tokens_max_mma(const T* __restrict__ dtok, int
     qv[c] = make_uint4(0, 0, 0, 0);
     if (c * 4 + t < nvec) qv[c] = __ldg(reinterpret_cast<const uint4*>(q) + c * 4 + t);
   }
-  if (wid < ntile) load_step(wid);  // the document's first rows are in flight while |q| is taken
   float nq2 = 0.0f;
 #pragma unroll
   for (int c = 0; c < KCMAX; ++c) {
@@ -830,6 +836,7 @@ __device__ __forceinline__ double tokens_max_mma(const T* __restrict__ dtok, int
   };
 
   for (int64_t tb = wid; tb < ntile; tb += stride) {  // warp-uniform
+    load_step(tb);
     float sv[BT][2];
 #pragma unroll
     for (int b = 0; b < BT; ++b) {
@@ -844,7 +851,6 @@ __device__ __forceinline__ double tokens_max_mma(const T* __restrict__ dtok, int
       sv[b][0] = acc[0];
       sv[b][1] = acc[2];
     }
-    if (tb + stride < ntile) load_step(tb + stride);  // the next step's rows fly during the bookkeeping below
     float ub[BT][2];
     float lbmax = -INFINITY;
 #pragma unroll
@@ -895,6 +901,192 @@ __device__ __forceinline__ double tokens_max_mma(const T* __restrict__ dtok, int
   return best;
 }
 
+#ifndef CBX_BD_STREAM_NOALLOC
+#define CBX_BD_STREAM_NOALLOC 1  // document tokens bypass L1 allocation (read once per reveal; L1 keeps the run's metadata)
+#endif
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+#if CBX_BD_STREAM_NOALLOC
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+// float64 dot of the 8 + 8 elements of two 16-byte vectors, k ascending from +0.0 (the exact pass's chain)
+template <typename T>
+__device__ __forceinline__ double vec_dot_exact(const uint4& w, const uint4& qw) {
+  const T* x = reinterpret_cast<const T*>(&w);
+  const T* y = reinterpret_cast<const T*>(&qw);
+  double part = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) part = fma(Elem<T>::to_d(x[k]), Elem<T>::to_d(y[k]), part);
+  return part;
+}
+// The exact float64 dot of a row held as KCMAX vectors per lane (vector index v = 4 c + t over the row's four
+// lanes t), summed in exactly the order of the one-vector-per-lane butterfly used everywhere else in this
+// file (xor 16, 8, 4, 2, 1 over v): the xor 16 / 8 / 4 levels pair vectors of the same lane (c ^ 4, c ^ 2,
+// c ^ 1; absent vectors are +0.0, as idle lanes are there), xor 2 and 1 are shuffles between the four lanes.
+template <typename T, int KCMAX>
+__device__ __forceinline__ double row_dot_exact(const uint4 (&r)[KCMAX], const uint4 (&qv)[KCMAX]) {
+  double P[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) P[c] = 0.0;
+#pragma unroll
+  for (int c = 0; c < KCMAX; ++c) P[c] = vec_dot_exact<T>(r[c], qv[c]);
+  double s;
+  if constexpr (KCMAX > 4) {
+    const double q0 = P[0] + P[4], q1 = P[1] + P[5], q2 = P[2] + P[6], q3 = P[3] + P[7];  // xor 16
+    s = (q0 + q2) + (q1 + q3);                                                           // xor 8, xor 4
+  } else if constexpr (KCMAX > 2) {
+    s = (P[0] + P[2]) + (P[1] + P[3]);  // xor 8, xor 4
+  } else if constexpr (KCMAX > 1) {
+    s = P[0] + P[1];  // xor 4
+  } else {
+    s = P[0];
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;
+}
+#ifndef CBX_BD_MMA_NOINLINE
+#define CBX_BD_MMA_NOINLINE 0  // 1: the register variant as a real call (measured no better: the call is merged back)
+#endif
+#if CBX_BD_MMA_NOINLINE
+#define CBX_BD_MMA_LINKAGE static __device__ __noinline__
+#else
+#define CBX_BD_MMA_LINKAGE __device__ __forceinline__
+#endif
+template <typename T, int KCMAX, int BT>
+CBX_BD_MMA_LINKAGE double tokens_max_mma(const T* __restrict__ dtok, int64_t j0, int64_t j1,
+                                                 const T* __restrict__ q, int dim, int wid, int nwarps, int lane,
+                                                 double best, unsigned int* shared_lb, float xmax) {
+  const int nvec = dim >> 3;        // 16-byte vectors per row
+  const int kc = (nvec + 3) >> 2;   // 64-byte chunks per row (the last one zero-padded when dim % 32 != 0)
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t ntile = (j1 - j0 + 15) >> 4;
+  const int64_t stride = (int64_t)nwarps * BT;
+  uint4 U[BT][KCMAX], V[BT][KCMAX];
+  // one step's loads: rows g and g + 8 of BT tiles (issued before anything that waits on data)
+  auto load_step = [&](int64_t tb) {
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+      const int64_t r0 = j0 + ((tb + (int64_t)b * nwarps) << 4) + g;
+      const uint4* p0 = reinterpret_cast<const uint4*>(dtok + r0 * dim) + t;
+      const uint4* p1 = reinterpret_cast<const uint4*>(dtok + (r0 + 8) * dim) + t;
+#pragma unroll
+      for (int c = 0; c < KCMAX; ++c) {
+        U[b][c] = make_uint4(0, 0, 0, 0);
+        V[b][c] = make_uint4(0, 0, 0, 0);
+        if (c * 4 + t < nvec && r0 < j1) U[b][c] = ld_stream(p0 + c * 4);
+        if (c * 4 + t < nvec && r0 + 8 < j1) V[b][c] = ld_stream(p1 + c * 4);
+      }
+    }
+  };
+  uint4 qv[KCMAX];
+#pragma unroll
+  for (int c = 0; c < KCMAX; ++c) {
+    qv[c] = make_uint4(0, 0, 0, 0);
+    if (c * 4 + t < nvec) qv[c] = __ldg(reinterpret_cast<const uint4*>(q) + c * 4 + t);
+  }
+  const bool have = wid < ntile;
+  if (have) load_step(wid);  // the document's first rows are in flight while |q| is taken
+  float nq2 = 0.0f;
+#pragma unroll
+  for (int c = 0; c < KCMAX; ++c) {
+    const T* x = reinterpret_cast<const T*>(&qv[c]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) nq2 = __fmaf_rn(Elem<T>::to_f(x[k]), Elem<T>::to_f(x[k]), nq2);
+  }
+  nq2 = __fadd_rn(nq2, __shfl_xor_sync(0xffffffffu, nq2, 1));
+  nq2 = __fadd_rn(nq2, __shfl_xor_sync(0xffffffffu, nq2, 2));
+  const bool screen = nq2 >= 0x1p-60f && nq2 <= 0x1p60f && xmax <= 0x1p60f;
+  const float qn = __fmul_ru(__fsqrt_ru(nq2), 1.0000005f);  // the fp32 |q|^2 above is within 2^-20 of the exact one
+  const float eps = __fmaf_ru(__fmul_ru(__fmul_ru(xmax, qn), (float)dim), 0x1p-19f, 0x1p-40f);
+  float LB = best == -INFINITY ? -INFINITY : __double2float_rd(best);
+  float ub[BT][2];
+
+  // rows that may hold the maximum (ub >= LB): their exact float64 dots, taken from the registers that hold
+  // the rows — all eight rows of a (tile, half) at once, one per lane group
+  auto resolve = [&]() {
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!__any_sync(0xffffffffu, !(ub[b][h] < LB))) continue;  // warp-uniform
+        const double e = h ? row_dot_exact<T, KCMAX>(V[b], qv) : row_dot_exact<T, KCMAX>(U[b], qv);
+        // max over the live rows (a dead row's ub is -inf; non-candidates cannot exceed the maximum anyway)
+        const uint64_t k = ub[b][h] == -INFINITY ? 0ull : ord_key(e);
+        const uint32_t kh = (uint32_t)(k >> 32);
+        const uint32_t mh = __reduce_max_sync(0xffffffffu, kh);
+        const uint32_t ml = __reduce_max_sync(0xffffffffu, kh == mh ? (uint32_t)k : 0u);
+        const uint64_t km = ((uint64_t)mh << 32) | ml;
+        if (km) {
+          const double m = ord_val(km);
+          if (m > best) {
+            best = m;
+            LB = fmaxf(LB, __double2float_rd(m));
+          }
+        }
+      }
+    }
+  };
+
+  int64_t tb = wid;
+  bool pending = false;  // the last step's rows wait for the CTA-wide bound
+  while (have) {  // warp-uniform
+    float lbmax = -INFINITY;
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int c = 0; c < KCMAX; ++c) {
+        if (c < kc) {
+          mma16816<T>(acc, U[b][c].x, V[b][c].x, U[b][c].y, V[b][c].y, qv[c].x, qv[c].y);
+          mma16816<T>(acc, U[b][c].z, V[b][c].z, U[b][c].w, V[b][c].w, qv[c].z, qv[c].w);
+        }
+      }
+      const int64_t r0 = j0 + ((tb + (int64_t)b * nwarps) << 4) + g;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float s = h ? acc[2] : acc[0];
+        const bool live = r0 + 8 * h < j1;
+        ub[b][h] = !live ? -INFINITY : (screen ? __fadd_ru(s, eps) : INFINITY);
+        const float lb = __fsub_rd(s, eps);
+        if (live && screen && lb <= 3.0e38f && lb >= -3.0e38f) lbmax = fmaxf(lbmax, lb);  // finite only
+      }
+    }
+    // LB over the warp (and, through shared_lb, over the CTA's warps so far)
+    const uint32_t lk = __reduce_max_sync(0xffffffffu, lbmax == -INFINITY ? 0u : ord_key_f(lbmax));
+    if (lk) LB = fmaxf(LB, ord_val_f(lk));
+    if (shared_lb) {
+      if (lane == 0 && lk) atomicMax(shared_lb, lk);
+      const uint32_t sk = *reinterpret_cast<volatile unsigned int*>(shared_lb);
+      if (sk) LB = fmaxf(LB, ord_val_f(sk));
+    }
+    if (tb + stride >= ntile) {
+      pending = true;
+      break;
+    }
+    resolve();  // before the registers take the next step's rows
+    tb += stride;
+    load_step(tb);
+  }
+  if (shared_lb) {
+    // every warp has published its rows' lower bounds: the exact pass only sees the document's front-runners
+    __syncthreads();
+    const uint32_t sk = *reinterpret_cast<volatile unsigned int*>(shared_lb);
+    if (sk) LB = fmaxf(LB, ord_val_f(sk));
+  }
+  if (pending) resolve();
+  return best;
+}
+
+#ifndef CBX_BD_MMA_REGS
+#define CBX_BD_MMA_REGS 0
+#endif
 #ifndef CBX_BD_MMA
 #define CBX_BD_MMA 1  // tensor-core (mma.sync) screen for 16-bit tokens with dim <= 256
 #endif
@@ -907,15 +1099,34 @@ __device__ __forceinline__ double tokens_max_mma(const T* __restrict__ dtok, int
 // maximum over tokens [j0, j1) of the float64 dot with q; `init` is the clamp floor.
 // (G, VPL) is the all-float64 layout; wid/nwarps/lane place the calling warp for the screened layout;
 // xmax bounds the document tokens' norms (screened layout).
-template <typename T, int G, int VPL, int B>
+// WBT > 0: the calling kernel owns its SM's register file (one CTA per SM, up to 255 registers per thread):
+// the tensor-core screen then stages WBT tiles per warp and step and takes the exact dots from the staging
+// registers (tokens_max_mma) — no second load of the front-runner rows.
+#ifndef CBX_BD_WIDE_BT
+#define CBX_BD_WIDE_BT 2  // 16-row tiles staged per warp and step in wide launches (d <= 128; 3 spills at 255 registers)
+#endif
+#ifndef CBX_BD_WARM_BT
+#define CBX_BD_WARM_BT 3  // the same in the warm-up pre-pass kernel (248 registers, no spills)
+#endif
+template <typename T, int G, int VPL>
+__host__ __device__ constexpr bool bd_mma_layout() { return sizeof(T) == 2 && CBX_BD_SCREEN && CBX_BD_MMA && G * VPL <= 32; }
+template <typename T, int G, int VPL, int B, int WBT = 0>
 __device__ __forceinline__ double tokens_max(const T* __restrict__ dtok, int64_t j0, int64_t j1, const T* q, int dim,
                                              int gid, int ngroups, int sub, double init, int wid, int nwarps,
                                              const unsigned long long* shared_best, unsigned int* shared_lb, float xmax) {
   if constexpr (sizeof(T) == 2 && CBX_BD_SCREEN) {
     if constexpr (CBX_BD_MMA && G * VPL <= 32) {
       constexpr int KCMAX = (G * VPL) / 4;
+      if constexpr (WBT > 0)  // WBT tiles per warp and step for d <= 128 (4 staging registers per tile and 32 dims)
+        return tokens_max_mma<T, KCMAX, (KCMAX <= 4 ? WBT : (WBT + 1) / 2)>(dtok, j0, j1, q, dim, wid, nwarps,
+                                                                            threadIdx.x & 31, init, shared_lb, xmax);
+#if CBX_BD_MMA_REGS
       return tokens_max_mma<T, KCMAX, (KCMAX <= 4 ? 2 : 1)>(dtok, j0, j1, q, dim, wid, nwarps, threadIdx.x & 31, init,
                                                              shared_lb, xmax);
+#else
+      return tokens_max_mma_reload<T, KCMAX, (KCMAX <= 4 ? 2 : 1)>(dtok, j0, j1, q, dim, wid, nwarps,
+                                                                    threadIdx.x & 31, init, shared_lb, xmax);
+#endif
     }
     constexpr int SG = (G * VPL) / 4 < 1 ? 1 : (G * VPL) / 4;
     return tokens_max_screen<T, SG, CBX_BD_SCREEN_B>(dtok, j0, j1, q, dim, wid, nwarps, threadIdx.x & 31, init,
@@ -937,12 +1148,20 @@ __device__ __forceinline__ double tokens_max(const T* __restrict__ dtok, int64_t
 // A compile-time placement lets every row/tree access be a plain LDS/STS (or LDG/STG) instead of a generic
 // load: generic loads that resolve to shared memory still queue in the SM's global-memory pipeline, behind
 // a co-resident CTA's reveal (measured: ~4.7k cycles of thread 0's row update per cfg2 iteration).
-template <typename T, int G, int VPL, int NT, bool UNI, int SM>
-__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const BanditParams P) {
-  // NT = 256: two runs per SM (register file split); NT = 512 when every run has an SM to itself:
-  // twice the warps for the reveal and the warm-up of one run
-  constexpr int BD_THREADS = NT;
-  constexpr int BD_WARPS = NT / 32;
+// threads per CTA: NT = 256 is two runs per SM (register file split, 128 registers per thread); NT = 512 is
+// the "wide" launch, every run with an SM to itself, in one of two shapes: 512 threads of 128 registers
+// (16 warps x 2 tiles = 512 rows per reveal step: long documents, cfg3's 1030 rows), or — WREG, tensor-core
+// screen only — 256 threads of up to 255 registers, whose reveal keeps its rows in registers for the exact
+// pass (8 warps x 2 tiles = 256 rows per step: documents of a few hundred rows, cfg4). The launcher picks by
+// the batch's mean document length.
+template <int NT, bool WREG>
+__host__ __device__ constexpr int bd_threads() { return NT == 512 && WREG ? 256 : NT; }
+template <typename T, int G, int VPL, int NT, bool UNI, int SM, bool WREG = false>
+__global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) bandit_kernel(const BanditParams P) {
+  static_assert(!WREG || (NT == 512 && bd_mma_layout<T, G, VPL>()), "WREG is a wide tensor-core-screen shape");
+  constexpr bool WIDE = WREG;  // rows stay in the staging registers for the exact pass
+  constexpr int BD_THREADS = bd_threads<NT, WREG>();
+  constexpr int BD_WARPS = BD_THREADS / 32;
   extern __shared__ __align__(16) uint8_t bd_smem[];
   constexpr int NGROUPS = BD_THREADS / G;
 #ifndef CBX_BD_TOKENS_IN_FLIGHT
@@ -1120,9 +1339,10 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
   // H[i, t] by one warp (warm-up cells)
   auto cell_warp = [&](int i, int t) -> double {
     if (!tokens) return P.matrix[(R.row_begin + i) * P.ld_matrix + t];
-    double best = tokens_max<T, GW, VPL, (VPL == 1 ? 8 : 4)>(dtok, dto[i], dto[i + 1], qtok + (int64_t)t * dim,
-                                                                   dim, lane / GW, 32 / GW, lane % GW, init_cell, 0, 1,
-                                                                   nullptr, nullptr, P.xmax);
+    double best = tokens_max<T, GW, VPL, (VPL == 1 ? 8 : 4), WIDE ? CBX_BD_WIDE_BT : 0>(dtok, dto[i], dto[i + 1],
+                                                                         qtok + (int64_t)t * dim, dim, lane / GW,
+                                                                         32 / GW, lane % GW, init_cell, 0, 1, nullptr,
+                                                                         nullptr, P.xmax);
 #pragma unroll
     for (int o = 16; o >= GW; o >>= 1) {
       const double w = __shfl_xor_sync(0xffffffffu, best, o);
@@ -1484,7 +1704,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) bandit_kernel(const Ban
 #else
       const int64_t j0 = dto[i_star], j1 = dto[i_star + 1];
 #endif
-      double best = tokens_max<T, G, VPL, B>(dtok, j0, j1, qtok + (int64_t)t_star * dim, dim,
+      double best = tokens_max<T, G, VPL, B, WIDE ? CBX_BD_WIDE_BT : 0>(dtok, j0, j1, qtok + (int64_t)t_star * dim, dim,
                                              gid, NGROUPS, sub, init_cell, warp, BD_WARPS, &ctrl->cellkey, &ctrl->lbkey,
                                              P.xmax);
 #pragma unroll
@@ -1683,8 +1903,9 @@ __global__ void __launch_bounds__(256) warm_cells_kernel(const BanditParams P, i
     const int i = P.trace_i[slot], t = P.trace_t[slot];
     const int64_t* dto = P.d_tok_off + R.row_begin;
     const T* q = static_cast<const T*>(P.q_tokens) + (P.q_tok_off[R.query] + t) * (int64_t)P.dim;
-    double best = tokens_max<T, GW, VPL, (VPL == 1 ? 8 : 4)>(dtok, dto[i], dto[i + 1], q, P.dim, lane / GW, 32 / GW,
-                                                             lane % GW, init_cell, 0, 1, nullptr, nullptr, P.xmax);
+    double best = tokens_max<T, GW, VPL, (VPL == 1 ? 8 : 4), CBX_BD_WARM_BT>(dtok, dto[i], dto[i + 1], q, P.dim, lane / GW,
+                                                                   32 / GW, lane % GW, init_cell, 0, 1, nullptr, nullptr,
+                                                                   P.xmax);
 #pragma unroll
     for (int o = 16; o >= GW; o >>= 1) {
       const double w = __shfl_xor_sync(0xffffffffu, best, o);
@@ -1697,8 +1918,16 @@ __global__ void __launch_bounds__(256) warm_cells_kernel(const BanditParams P, i
 #ifndef CBX_BD_WIDE
 #define CBX_BD_WIDE 1  // 512-thread CTAs when the runs fit one per SM
 #endif
+#ifndef CBX_BD_WREG_MAX_MEAN_ROWS
+#define CBX_BD_WREG_MAX_MEAN_ROWS 320  // wide launches: the 256-thread register shape up to this mean document length
+#endif
 template <typename T, int G, int VPL, bool UNI>
-static void (*pick_bandit(bool wide, int sm))(const BanditParams) {
+static void (*pick_bandit(bool wide, int sm, bool wreg))(const BanditParams) {
+  if constexpr (bd_mma_layout<T, G, VPL>()) {
+    if (wide && wreg)
+      return sm == 2 ? bandit_kernel<T, G, VPL, 512, UNI, 2, true>
+                     : (sm == 1 ? bandit_kernel<T, G, VPL, 512, UNI, 1, true> : bandit_kernel<T, G, VPL, 512, UNI, 0, true>);
+  }
   if (wide) return sm == 2 ? bandit_kernel<T, G, VPL, 512, UNI, 2>
                            : (sm == 1 ? bandit_kernel<T, G, VPL, 512, UNI, 1> : bandit_kernel<T, G, VPL, 512, UNI, 0>);
   return sm == 2 ? bandit_kernel<T, G, VPL, 256, UNI, 2> : bandit_kernel<T, G, VPL, 256, UNI, 0>;
@@ -1708,9 +1937,11 @@ template <typename T, int G, int VPL>
 static int launch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, cudaStream_t st) {
   const bool wide = CBX_BD_WIDE && n_runs <= sm_count();
   const int sm = P.use_smem ? 2 : (P.trees_smem ? 1 : 0);  // trees_smem is only set for wide launches
-  auto kern = pick_bandit<T, G, VPL, false>(wide, sm);
+  const bool wreg = bd_mma_layout<T, G, VPL>() && P.q_tokens != nullptr && P.mean_doc_rows <= CBX_BD_WREG_MAX_MEAN_ROWS;
+  const unsigned threads = wide ? (wreg ? 256 : 512) : 256;
+  auto kern = pick_bandit<T, G, VPL, false>(wide, sm, wreg);
   if constexpr (sizeof(T) == 2) {  // the BASELINE configs: 16-bit tokens with generic bounds
-    if (P.bounds_lo == nullptr) kern = pick_bandit<T, G, VPL, true>(wide, sm);
+    if (P.bounds_lo == nullptr) kern = pick_bandit<T, G, VPL, true>(wide, sm, wreg);
   }
   CBX_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (P.mbox && n_runs > 1) {
@@ -1718,11 +1949,11 @@ static int launch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, cud
     BanditParams Pc = P;
     void* args[] = {&Pc};
     cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3((unsigned)n_runs),
-                                                dim3(wide ? 512 : 256), args, smem, st);
+                                                dim3(threads), args, smem, st);
     if (e != cudaSuccess) return fail(CBX_ECUDA, std::string("bandit_kernel cooperative launch: ") + cudaGetErrorString(e));
     return CBX_OK;
   }
-  kern<<<(unsigned)n_runs, wide ? 512 : 256, smem, st>>>(P);
+  kern<<<(unsigned)n_runs, threads, smem, st>>>(P);
   CBX_LAUNCH_CHECK("bandit_kernel launch");
   return CBX_OK;
 }

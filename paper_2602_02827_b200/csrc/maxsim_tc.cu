@@ -539,14 +539,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 // ----------------------------------------------------------------- document-tile scorer (resident corpus)
 // The reranking service's scorer: the candidates of every query are scored in place in an HBM-resident
-// corpus (colbandit/oracle.py:205-227 for candidate lists). A tile is up to DT_ROWS consecutive rows of ONE
-// document, loaded where it lies by one TMA box per K block (box heights 8, 16, ..., DT_ROWS rows: at most
-// 7 rows of over-read per tile) and multiplied with N = ceil16(rows): no packed layout, no per-tile document
-// walk in the producer, no segment logic in the epilogue. Same roles and barriers as maxsim_tc_kernel;
-// a document longer than one tile hands its running max to the next tile through the carry chain.
-constexpr int DT_ROWS = 128;
+// corpus (colbandit/oracle.py:205-227 for candidate lists). A tile is up to TR consecutive rows of ONE
+// document (TR = 256 for d <= 128, 128 for d <= 256), loaded where it lies by one TMA box per K block (box
+// heights 8, 16, ..., TR rows: at most 7 rows of over-read per tile) and multiplied with N = ceil16(rows):
+// no packed layout, no per-tile document walk in the producer, no segment logic in the epilogue. Same roles
+// and barriers as maxsim_tc_kernel; a document longer than one tile hands its running max to the next tile
+// through the carry chain. The producer and the MMA issuer are single instruction streams, and at ~100
+// instructions per tile they — not HBM — bound the first version of this kernel (128-row tiles, ncu:
+// profiles/r2_ncu_docs_v2_cfg2_lines.txt); 256-row tiles cut the tiles per document from 1.87 to 1.17 on cfg2.
+constexpr int DT_MAX_ROWS = 256;
+constexpr int DT_SLOTS = 16;  // tiles in flight (barrier pairs); their bytes share one ring
 struct DocTmaps {
-  CUtensorMap d[DT_ROWS / 8];  // d[h - 1]: boxes of 8 h rows x 64 columns
+  CUtensorMap d[DT_MAX_ROWS / 8];  // d[h - 1]: boxes of 8 h rows x 64 columns
   CUtensorMap q;
 };
 
@@ -588,14 +592,12 @@ struct DocWindow {
   __device__ __forceinline__ int64_t source(int64_t d) const { return __shfl_sync(0xffffffffu, src, (int)(d - win)); }
 };
 
-constexpr int DT_SLOTS = 16;  // tiles in flight (barrier pairs); their bytes share one ring
 __global__ void __launch_bounds__(TC_THREADS, 1)
     maxsim_docs_kernel(const __grid_constant__ DocTmaps tm, TcParams p) {
   // Shared memory: the query operand, then ONE byte ring for the document tiles: a tile of h rows takes
   // ceil8(h) x 128 B per K block, placed right behind its predecessor (wrapping to 0 when it would cross the
-  // end), so the ring holds ~40 % more bytes in flight than fixed 128-row stages do on ragged documents —
-  // the stream is latency bound, bytes in flight are bandwidth. Placement is a pure function of the tile
-  // sizes, so the MMA warp recomputes it; the producer alone tracks what has been consumed.
+  // end). Placement is a pure function of the tile sizes, so the MMA warp recomputes it; the producer alone
+  // tracks what has been consumed (virtual ring positions of the tiles in flight, one per lane).
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* q_slot = smem;                                    // kblocks x (128 rows x 128 B)
@@ -612,10 +614,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cfull + TC_ACC_BUFS);
   float* carry = reinterpret_cast<float*>(bars + 64);        // [4 slots][4 warps][32]
   float* part = carry + 4 * 4 * 32;                          // [2 parity][4 quads]
-  uint64_t* vstart = reinterpret_cast<uint64_t*>(part + 8);  // [DT_SLOTS] virtual ring position of each tile in flight
   static_assert(2 * DT_SLOTS + 2 + 3 * TC_ACC_BUFS + 1 <= 64, "barrier block");
+  static_assert(DT_SLOTS <= 32, "one lane per tile in flight");
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int TR = p.tile_n;                     // tile rows: 128 or 256
+  // TMEM accumulators: 4 x 128 or 2 x 256 columns. The accumulator barriers are always a ring of four
+  // (index tg & 3): with rep = 4 a group meets every fourth tile, and a barrier that also completed for
+  // another group's tile in between would put the waiter two phases behind (parity aliasing).
+  const uint32_t nacc = 512u / (uint32_t)TR, accmask = nacc - 1u;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < DT_SLOTS; ++s) {
@@ -631,25 +638,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     ptx::fence_mbarrier_init();
   }
-  if (warp == 0 && lane < DT_ROWS / 8) ptx::prefetch_tmap(&tm.d[lane]);
-  if (warp == 0 && lane == 31) ptx::prefetch_tmap(&tm.q);
-  if (warp == 1) ptx::tmem_alloc<TC_ACC_BUFS * TC_MAX_TILE_N>(tmem_holder);
+  if (warp == 0 && lane < TR / 8) ptx::prefetch_tmap(&tm.d[lane]);
+  if (warp == 2 && lane == 0) ptx::prefetch_tmap(&tm.q);
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_holder);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (lane 0 issues)
+    // ------------------------------------------------------------ TMA producer
+    // every lane runs the same stream (no divergent sections); lane 0 arms the barriers and issues the copies
     uint32_t qphase = 0, tg = 0, tail = 0, off = 0;
-    uint64_t vpos = 0;
+    uint64_t vpos = 0, vs = 0;  // vs: virtual ring position of the tile in flight in slot `lane`
     const uint64_t pol = ptx::policy_evict_first();
     ChunkCursor cur;
     cur.init(p);
     ChunkInfo c;
     while (cur.next(p, c)) {
+      ptx::mbar_wait(qempty, qphase ^ 1);
       if (lane == 0) {
-        ptx::mbar_wait(qempty, qphase ^ 1);
         ptx::mbar_arrive_expect_tx(qfull, (uint32_t)(p.rep * p.kblocks * p.lqp * 128));
         for (int g = 0; g < p.rep; ++g)
           for (int kb = 0; kb < p.kblocks; ++kb)
@@ -661,35 +669,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int64_t d = c.doc0; d < c.doc1; ++d) {
         w.seek(d, lane);
         const int32_t len = w.length(d);
-        const int64_t src = w.source(d);
-        if (lane == 0) {
-          for (int32_t r = 0; r < len; r += DT_ROWS, ++tg) {
-            const int h8 = ((len - r < DT_ROWS ? len - r : DT_ROWS) + 7) >> 3;  // box height / 8
-            const uint32_t kbytes = (uint32_t)h8 * 1024u, S = kbytes * (uint32_t)p.kblocks;
-            if (off + S > C) {  // the tile would cross the ring's end: it starts over at 0
-              vpos += C - off;
-              off = 0;
-            }
-            // tiles are consumed in order: wait for the oldest ones until none overlaps [vpos, vpos + S)
-            // (tile j overlaps iff its start is less than a ring length behind this tile's end)
-            while (tail < tg && (tg - tail == DT_SLOTS || vstart[tail % DT_SLOTS] + C < vpos + S)) {
-              ptx::mbar_wait(&empty[tail % DT_SLOTS], (tail / DT_SLOTS) & 1u);
-              ++tail;
-            }
-            const uint32_t slot = tg % DT_SLOTS;
-            vstart[slot] = vpos;
+        const int32_t src = (int32_t)w.source(d);
+        for (int32_t r = 0; r < len; r += TR, ++tg) {
+          const int h8 = ((len - r < TR ? len - r : TR) + 7) >> 3;  // box height / 8
+          const uint32_t kbytes = (uint32_t)h8 * 1024u, S = kbytes * (uint32_t)p.kblocks;
+          if (off + S > C) {  // the tile would cross the ring's end: it starts over at 0
+            vpos += C - off;
+            off = 0;
+          }
+          // tiles are consumed in order: wait for the oldest ones until none overlaps [vpos, vpos + S)
+          // (tile j overlaps iff its start is less than a ring length behind this tile's end)
+          while (tail < tg) {
+            const uint64_t vt = __shfl_sync(0xffffffffu, vs, (int)(tail % DT_SLOTS));
+            if (tg - tail < DT_SLOTS && vt + C >= vpos + S) break;
+            ptx::mbar_wait(&empty[tail % DT_SLOTS], (tail / DT_SLOTS) & 1u);
+            ++tail;
+          }
+          const uint32_t slot = tg % DT_SLOTS;
+          if (lane == (int)slot) vs = vpos;
+          if (lane == 0) {
             ptx::mbar_arrive_expect_tx(&full[slot], S);
             for (int kb = 0; kb < p.kblocks; ++kb)
-              ptx::tma_load_2d_hint(ring + off + kb * kbytes, &tm.d[h8 - 1], &full[slot], kb * 64,
-                                    (int32_t)(src + r), pol);
-            off += S;
-            vpos += S;
+              ptx::tma_load_2d_hint(ring + off + kb * kbytes, &tm.d[h8 - 1], &full[slot], kb * 64, src + r, pol);
           }
+          off += S;
+          vpos += S;
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (lane 0 issues)
+    // ------------------------------------------------------------ MMA issuer (lane 0 issues; every lane runs the stream)
     uint32_t qphase = 0, tg = 0, off = 0;
     ChunkCursor cur;
     cur.init(p);
@@ -697,33 +706,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t q_addr = ptx::smem_u32(q_slot);
     const uint32_t ring_addr = ptx::smem_u32(ring);
     const uint64_t ad0 = ptx::smem_desc_sw128(q_addr);
+    const uint64_t bd_ring = ptx::smem_desc_sw128(ring_addr);  // start-address field advances by off >> 4
     const uint32_t idesc0 = p.idesc & ~(0x3Fu << 17);  // N field cleared
     while (cur.next(p, c)) {
-      if (lane == 0) {
-        ptx::mbar_wait(qfull, qphase);
-        ptx::tc_fence_after();
-      }
+      ptx::mbar_wait(qfull, qphase);
+      ptx::tc_fence_after();
       qphase ^= 1;
       DocWindow w;
       w.open(p, c.doc0, c.doc1, lane, false);
       for (int64_t d = c.doc0; d < c.doc1; ++d) {
         w.seek(d, lane);
         const int32_t len = w.length(d);
-        if (lane == 0) {
-          for (int32_t r = 0; r < len; r += DT_ROWS, ++tg) {
-            const int32_t h = len - r < DT_ROWS ? len - r : DT_ROWS;
-            const uint32_t kbytes = (uint32_t)((h + 7) >> 3) * 1024u, S = kbytes * (uint32_t)p.kblocks;
-            if (off + S > C) off = 0;  // the producer's placement rule
-            const uint32_t idesc = idesc0 | ((uint32_t)(((h + 15) >> 4) * 2) << 17);
-            const uint32_t acc = tg & (TC_ACC_BUFS - 1), slot = tg % DT_SLOTS;
-            ptx::mbar_wait(&tempty[acc], ((tg >> 2) & 1) ^ 1);
-            ptx::mbar_wait(&full[slot], (tg / DT_SLOTS) & 1u);
-            ptx::tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * TC_MAX_TILE_N;
-            const uint64_t bd0 = ptx::smem_desc_sw128(ring_addr + off);
+        for (int32_t r = 0; r < len; r += TR, ++tg) {
+          const int32_t h = len - r < TR ? len - r : TR;
+          const uint32_t kbytes = (uint32_t)((h + 7) >> 3) * 1024u, S = kbytes * (uint32_t)p.kblocks;
+          if (off + S > C) off = 0;  // the producer's placement rule
+          const uint32_t idesc = idesc0 | ((uint32_t)(((h + 15) >> 4) * 2) << 17);
+          const uint32_t acc = tg & accmask, slot = tg % DT_SLOTS;
+          if (tg >= nacc) ptx::mbar_wait(&tempty[(tg - nacc) & 3], ((tg - nacc) >> 2) & 1);  // accumulator drained
+          ptx::mbar_wait(&full[slot], (tg / DT_SLOTS) & 1u);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t d_tmem = tmem_base + acc * (uint32_t)TR;
+            const uint64_t bd0 = bd_ring + (uint64_t)(off >> 4);
             const uint32_t bstep = kbytes >> 4;
 #pragma unroll
-            for (int kb = 0; kb < 8; ++kb) {
+            for (int kb = 0; kb < 4; ++kb) {
               if (kb >= p.kblocks) break;
 #pragma unroll
               for (int k4 = 0; k4 < 4; ++k4)
@@ -731,12 +739,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                 idesc, (kb | k4) != 0);
             }
             ptx::tc_commit(&empty[slot]);
-            ptx::tc_commit(&tfull[acc]);
-            off += S;
+            ptx::tc_commit(&tfull[tg & 3]);
           }
+          __syncwarp();
+          off += S;
         }
       }
       if (lane == 0) ptx::tc_commit(qempty);
+      __syncwarp();
     }
   } else if (warp >= TC_EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
@@ -760,27 +770,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int64_t d = c.doc0; d < c.doc1; ++d) {
           w.seek(d, lane);
           const int32_t len = w.length(d);
-          for (int32_t r = 0; r < len; r += DT_ROWS, ++tg) {
+          for (int32_t r = 0; r < len; r += TR, ++tg) {
             if ((int)(tg % (uint32_t)rep) != grp) continue;
-            const int ncols = len - r < DT_ROWS ? len - r : DT_ROWS;
-            const uint32_t acc = tg & (TC_ACC_BUFS - 1);
-            ptx::mbar_wait(&tfull[acc], (tg >> 2) & 1);
+            const int ncols = len - r < TR ? len - r : TR;
+            const uint32_t acc = tg & accmask;
+            ptx::mbar_wait(&tfull[tg & 3], (tg >> 2) & 1);
             ptx::tc_fence_after();
-            float v[DT_ROWS / 32][32];
-            const uint32_t taddr = tmem_base + tmem_lane + acc * TC_MAX_TILE_N;
-#pragma unroll
-            for (int b = 0; b < DT_ROWS / 32; ++b)
-              if (b * 32 < ncols) ptx::tmem_ld_32x32b_x32(taddr + b * 32, v[b]);
-            ptx::tmem_ld_wait();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            const uint32_t taddr = tmem_base + tmem_lane + acc * (uint32_t)TR;
             float cur = init;
+            for (int c0 = 0; c0 < ncols; c0 += 128) {  // 128 columns at a time (the registers' worth)
+              float v[4][32];
 #pragma unroll
-            for (int b = 0; b < DT_ROWS / 32; ++b) {
-              if (b * 32 >= ncols) break;
-              if (ncols - b * 32 >= 32) cur = fmaxf(cur, max32(v[b]));
-              else cur = masked_max(v[b], 0, ncols - b * 32, cur);
+              for (int b = 0; b < 4; ++b)
+                if (c0 + b * 32 < ncols) ptx::tmem_ld_32x32b_x32(taddr + c0 + b * 32, v[b]);
+              ptx::tmem_ld_wait();
+              if (c0 + 128 >= ncols) {  // the accumulator is read out: hand it back before the arithmetic
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[tg & 3]);
+              }
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                const int left = ncols - c0 - b * 32;
+                if (left <= 0) break;
+                if (left >= 32) cur = fmaxf(cur, max32(v[b]));
+                else cur = masked_max(v[b], 0, left, cur);
+              }
             }
             // carry chain (every tile waits for its predecessor's publication: keeps slot reuse ordered)
             float p_prev = init;
@@ -793,7 +808,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             carry[((tg & 3) * 4 + wig) * 32 + lane] = cur;
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&cfull[tg & 3]);
-            if (r + DT_ROWS >= len) {  // the document's last tile
+            if (r + TR >= len) {  // the document's last tile
               const float x = warp_sum(lane_valid ? cur : 0.0f);
               if (nq == 1) {
                 if (lane == 0) p.scores[d] = x;
@@ -818,7 +833,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<TC_ACC_BUFS * TC_MAX_TILE_N>(tmem_base);
+    ptx::tmem_dealloc<512>(tmem_base);
   }
 }
 
@@ -1087,25 +1102,26 @@ int launch_maxsim_tc_packed(const cbx_batch* b, const int64_t* corpus_off, int64
   plan_add_kernel<<<(unsigned)nb, PL_THREADS, 0, stream>>>(pk, n, btot, nb);
   CBX_LAUNCH_CHECK("plan_add_kernel launch");
   TcLaunch L;
-  int rc = prepare_tc(b, b->d_tokens, b->n_d_tokens, scores, L, docs ? DT_ROWS : CBX_PK_TILE_N);
+  int rc = prepare_tc(b, b->d_tokens, b->n_d_tokens, scores, L, docs ? 128 : CBX_PK_TILE_N);
   if (rc) return rc;
   L.p.packed = 1;
   if (docs) {
-    // one tile = up to DT_ROWS rows of one document; CTAs own balanced ranges of the ceil8(len) prefix
-    static_assert(DT_ROWS == 128, "stage layout and TMEM buffers are sized for 128-row tiles");
+    // one tile = up to TR rows of one document; CTAs own balanced ranges of the ceil8(len) prefix
+    const int TR = L.p.kblocks <= 2 ? 256 : 128;  // a tile's K blocks must leave the ring room for several tiles
     DocTmaps tm;
-    for (int h = 1; h <= DT_ROWS / 8; ++h) {
+    for (int h = 1; h <= DT_MAX_ROWS / 8; ++h) {
       rc = make_tmap(&tm.d[h - 1], b->d_tokens, b->dtype, b->n_d_tokens, b->dim, (uint32_t)(8 * h));
       if (rc) return rc;
     }
     tm.q = L.tm.q;
     {
       // one byte ring instead of fixed stages: everything the barrier block and the query operand leave
-      const size_t bar_bytes = 512 + (4 * 4 * 32 + 8) * sizeof(float) + DT_SLOTS * sizeof(uint64_t);
+      const size_t bar_bytes = 512 + (4 * 4 * 32 + 8) * sizeof(float);
       const size_t ring = (227 * 1024 - 1024 /*align slack*/ - bar_bytes - L.p.q_slot_bytes - 1024 /*over-read*/) &
                           ~size_t(1023);
       L.p.stages = 1;
       L.p.stage_bytes = (uint32_t)ring;
+      L.p.tile_n = TR;
       L.smem = 1024 + (size_t)L.p.q_slot_bytes + ring + 1024 + bar_bytes;
     }
     L.p.d_tok_off = pk;
