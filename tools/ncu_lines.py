@@ -77,7 +77,9 @@ def main():
         f, no = ln.split(":") if ":" in ln else (None, None)
         text = ""
         if f:
-            path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2602_02827_b200", "csrc", f)
+            # SRC_ROOT: the checkout the profiled library was built from (default: this one)
+            root = os.environ.get("SRC_ROOT", os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+            path = os.path.join(root, "paper_2602_02827_b200", "csrc", f)
             if path not in src and os.path.exists(path):
                 src[path] = open(path).read().splitlines()
             if path in src:
