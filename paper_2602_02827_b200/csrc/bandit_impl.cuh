@@ -1521,6 +1521,7 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
     BD_PHASE(0);
     if (warp == 0) {
       int wsel_i = -1;
+      int pf_row = -1;  // the row about to be revealed (rows in global memory: its lines are prefetched below)
       ColMask wsel_un{0ull, 0ull};
       Cand f[4];
       if (use_tree) {
@@ -1589,6 +1590,7 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
               wsel_un = un;
             }
             ctrl->i_star = i_star;
+            pf_row = i_star;
             ctrl->t_star = t_star;
             ctrl->cellkey = ord_key(init_cell);
             ctrl->lbkey = 0u;
@@ -1616,6 +1618,37 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
           }
         }
         ctrl->action = action;
+      }
+#ifndef CBX_BD_ROW_PREFETCH
+#define CBX_BD_ROW_PREFETCH 1
+#endif
+      if constexpr (SM != 2 && CBX_BD_ROW_PREFETCH) {
+        // rows live in global memory (pools above BD_SMEM_ROWS): one lane per line pulls what the row update,
+        // the membership test and the tree-leaf refresh of i* will read into L1 while the reveal runs (the
+        // reveal's own token loads do not allocate in L1 in the wide register shape)
+        const int pr = __shfl_sync(0xffffffffu, pf_row, 0);
+        if (pr >= 0) {
+          const int g0 = pr & ~31, g1 = min(g0 + 31, N - 1);
+          const void* a = nullptr;
+          switch (lane) {
+            case 0: a = rv.cnt + pr; break;
+            case 1: a = rv.mean + pr; break;
+            case 2: a = rv.m2 + pr; break;
+            case 3: a = rv.fx + pr; break;
+            case 4: a = rv.unrev_lo + pr; break;
+            case 5: a = rv.unrev_hi + pr; break;
+            case 6: a = rv.exp_mode + pr; break;
+            case 7: a = rv.member + g0; break;
+            case 8: a = rv.lcb + g0; break;
+            case 9: a = rv.lcb + g1; break;
+            case 10: a = rv.ucb + g0; break;
+            case 11: a = rv.ucb + g1; break;
+            case 12: a = rv.proxy + g0; break;
+            case 13: a = rv.proxy + g1; break;
+            default: break;
+          }
+          if (a) asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+        }
       }
       const int wi = uniform ? -1 : __shfl_sync(0xffffffffu, wsel_i, 0);
       if (wi >= 0) {  // one column per lane, warp argmax, ties to the lowest column (select_token, bandit.py:116-136)

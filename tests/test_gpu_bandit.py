@@ -382,3 +382,49 @@ def test_wide_queries_up_to_128_tokens_match_the_oracle():
         cells = maxsim_ref.cell_matrix(W.to_float64(qb, "bf16"), [t64[off[i]:off[i + 1]] for i in range(60)])
         ref = bandit_ref.run(cells, -1.0, 1.0, 5, alpha_ef=0.2, seed=(0, q))
         assert got[q].reveals == ref.reveals and got[q].topk == ref.topk
+
+
+def test_expansion_path_with_fp32_tokens_and_off_grid_bounds():
+    """The Shewchuk-expansion exact sums (values off the 2^-48 grid): fp32 tokens give cells that are multiples
+    of 2^-298 below 2^10, so any exact sum of them fits 6 non-overlapping doubles (capacity 8 is unreachable
+    for token sources); the per-cell bounds here are arbitrary float64 (off every grid). The oracle is fed
+    the device's own float64 cells (fp32 sums depend on the summation order, see the test above), so the
+    traces must be identical reveal for reveal."""
+    from paper_2602_02827_b200 import BanditConfig, BanditJob, CellBounds, run_batch
+    from paper_2602_02827_b200.batch import TokenBatch, exact_cells
+
+    cases = [W.gen_query("cfg1", q) for q in range(3)]
+    b = TokenBatch.from_host([c.query for c in cases], [case_doc_list(c) for c in cases], clamp_negative=False)
+    cells_all = exact_cells(b, with_scores=False)[0].cpu().numpy()
+    rng = np.random.default_rng(7)
+    jobs, refs, off = [], [], 0
+    for q, c in enumerate(cases):
+        T = c.query.shape[0]
+        cells = np.ascontiguousarray(cells_all[off:off + c.n_docs, :T])
+        lo = cells - rng.uniform(1e-9, 0.6, size=cells.shape) * rng.choice([1.0, 1e-7, 1e-14], size=cells.shape)
+        hi = cells + rng.uniform(1e-9, 0.6, size=cells.shape) * rng.choice([1.0, 1e-7, 1e-14], size=cells.shape)
+        cfg = BanditConfig(k=5, alpha_ef=(1.0, 0.3, 0.05)[q], seed=(3, q))
+        jobs.append(BanditJob(cfg, c.n_docs, T, q, off, CellBounds(lo, hi)))
+        refs.append(bandit_ref.run(cells, lo, hi, 5, alpha_ef=cfg.alpha_ef, seed=(3, q)))
+        off += c.n_docs
+    for got, ref in zip(run_batch(jobs, batch=b), refs):
+        assert got.reveals == ref.reveals and got.topk == ref.topk and got.iterations == ref.iterations
+
+
+def test_expansion_capacity_overflow_raises_instead_of_returning_a_wrong_sum():
+    """A matrix-backed oracle may hold any float64: values spread over ~900 binary orders need more than the 8
+    partials an expansion holds; the device run must either match the oracle or raise RuntimeError."""
+    from paper_2602_02827_b200 import BanditConfig, CellBounds, MaxSimOracle, run
+
+    rng = np.random.default_rng(11)
+    n, t = 6, 16
+    matrix = rng.uniform(0.5, 1.0, size=(n, t)) * np.exp2(-60.0 * np.arange(t))[None, :]
+    lo, hi = np.zeros((n, t)), np.full((n, t), 1.0)
+    ref = bandit_ref.run(matrix, lo, hi, 2, epsilon=1.0, seed=1)
+    try:
+        got = run(MaxSimOracle.from_matrix(matrix, value_range=(0.0, 1.0)), CellBounds(lo, hi),
+                  BanditConfig(k=2, epsilon=1.0, seed=1))
+    except RuntimeError as e:
+        assert "expansion" in str(e) or "exact" in str(e), e
+    else:
+        assert got.reveals == ref.reveals and got.topk == ref.topk
