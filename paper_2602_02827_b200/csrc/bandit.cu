@@ -359,6 +359,18 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
     }
   }
 
+  // the run's document offsets beside its rows, when that keeps the launch's occupancy (two CTAs per SM below
+  // 113 KB each, one above)
+  P.dto_smem_off = 0;
+  if (P.use_smem && b) {
+    const size_t off = align_up(smem, 16), need = (size_t)(max_rows + 1) * sizeof(int64_t);
+    const size_t cap = smem > 113 * 1024 || n_runs <= sm_count() ? 220 * 1024 : 113 * 1024;
+    if (off + need <= cap) {
+      P.dto_smem_off = (int64_t)off;
+      smem = off + need;
+    }
+  }
+
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int dt = b ? b->dtype : CBX_F64;
   const int dim = b ? b->dim : 16;

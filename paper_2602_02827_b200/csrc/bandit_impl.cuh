@@ -126,6 +126,7 @@ struct BanditParams {
   int trees_smem;      // rows global, selection trees in shared memory (set by the host when they fit)
   int bounds_smem;     // expansions (+ per-cell bounds) in shared memory at byte offset bounds_smem_off
   int64_t bounds_smem_off;
+  int64_t dto_smem_off;  // > 0: the run's document offsets (n_rows + 1 int64) are staged in shared memory there
   int32_t* topk;
   int32_t max_k;
   int32_t* trace_i;
@@ -1264,6 +1265,15 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
     dto = P.d_tok_off + R.row_begin;
   }
   const double init_cell = P.clamp_negative ? 0.0 : -INFINITY;
+  // the decision reads the token ranges of both boundary rows every iteration: from shared memory when the
+  // run's offsets fit there (an L2 round trip per iteration otherwise)
+  const int64_t* dto_s = nullptr;
+  if (SM == 2 && tokens && P.dto_smem_off > 0) {
+    int64_t* d = reinterpret_cast<int64_t*>(bd_smem + P.dto_smem_off);
+    for (int i = tid; i <= N; i += BD_THREADS) d[i] = dto[i];
+    dto_s = d;
+    __syncthreads();
+  }
 
   // optional phase cycle counters (thread 0; cbx_bandit_set_profile)
   unsigned long long ph[16] = {0};
@@ -1549,10 +1559,11 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
         // both candidates' token ranges come with the same round trip, so the reveal does not pay one
         int64_t jp0 = 0, jp1 = 0, jm0 = 0, jm1 = 0;
         if (tokens) {
-          jp0 = dto[i_plus];
-          jp1 = dto[i_plus + 1];
-          jm0 = dto[im];
-          jm1 = dto[im + 1];
+          const int64_t* o = (SM == 2 && dto_s) ? dto_s : dto;
+          jp0 = o[i_plus];
+          jp1 = o[i_plus + 1];
+          jm0 = o[im];
+          jm1 = o[im + 1];
         }
 #endif
         int action;
@@ -1620,7 +1631,7 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
         ctrl->action = action;
       }
 #ifndef CBX_BD_ROW_PREFETCH
-#define CBX_BD_ROW_PREFETCH 1
+#define CBX_BD_ROW_PREFETCH 0  // measured on cfg4: decide 1.9k -> 4.5k cycles, 1.79 -> 2.15 s (the prefetches queue in front of the decision); off
 #endif
       if constexpr (SM != 2 && CBX_BD_ROW_PREFETCH) {
         // rows live in global memory (pools above BD_SMEM_ROWS): one lane per line pulls what the row update,
@@ -1956,7 +1967,7 @@ __global__ void __launch_bounds__(256) warm_cells_kernel(const BanditParams P, i
 #endif
 template <typename T, int G, int VPL, bool UNI>
 static void (*pick_bandit(bool wide, int sm, bool wreg))(const BanditParams) {
-  if constexpr (bd_mma_layout<T, G, VPL>()) {
+  if constexpr (bd_mma_layout<T, G, VPL>() && G * VPL <= 16) {
     if (wide && wreg)
       return sm == 2 ? bandit_kernel<T, G, VPL, 512, UNI, 2, true>
                      : (sm == 1 ? bandit_kernel<T, G, VPL, 512, UNI, 1, true> : bandit_kernel<T, G, VPL, 512, UNI, 0, true>);
@@ -1968,9 +1979,13 @@ static void (*pick_bandit(bool wide, int sm, bool wreg))(const BanditParams) {
 
 template <typename T, int G, int VPL>
 static int launch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, cudaStream_t st) {
-  const bool wide = CBX_BD_WIDE && n_runs <= sm_count();
-  const int sm = P.use_smem ? 2 : (P.trees_smem ? 1 : 0);  // trees_smem is only set for wide launches
-  const bool wreg = bd_mma_layout<T, G, VPL>() && P.q_tokens != nullptr && P.mean_doc_rows <= CBX_BD_WREG_MAX_MEAN_ROWS;
+  // wide: every CTA has an SM to itself — because the runs fit one per SM, or because a run's shared-memory
+  // state (pools of ~1600 rows and more) leaves no room for a second CTA anyway (cfg5: 2000 rows)
+  const bool wide = CBX_BD_WIDE && (n_runs <= sm_count() || smem > 113 * 1024);
+  const int sm = P.use_smem ? 2 : (P.trees_smem ? 1 : 0);  // trees_smem is only set when the runs fit one per SM
+  // the register shape stages one tile per warp and step above d = 128 (and spills there): d <= 128 only
+  const bool wreg = bd_mma_layout<T, G, VPL>() && G * VPL <= 16 && P.q_tokens != nullptr &&
+                    P.mean_doc_rows <= CBX_BD_WREG_MAX_MEAN_ROWS;
   const unsigned threads = wide ? (wreg ? 256 : 512) : 256;
   auto kern = pick_bandit<T, G, VPL, false>(wide, sm, wreg);
   if constexpr (sizeof(T) == 2) {  // the BASELINE configs: 16-bit tokens with generic bounds

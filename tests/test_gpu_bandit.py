@@ -384,30 +384,34 @@ def test_wide_queries_up_to_128_tokens_match_the_oracle():
         assert got[q].reveals == ref.reveals and got[q].topk == ref.topk
 
 
-def test_expansion_path_with_fp32_tokens_and_off_grid_bounds():
-    """The Shewchuk-expansion exact sums (values off the 2^-48 grid): fp32 tokens give cells that are multiples
-    of 2^-298 below 2^10, so any exact sum of them fits 6 non-overlapping doubles (capacity 8 is unreachable
-    for token sources); the per-cell bounds here are arbitrary float64 (off every grid). The oracle is fed
-    the device's own float64 cells (fp32 sums depend on the summation order, see the test above), so the
-    traces must be identical reveal for reveal."""
+def test_expansion_path_with_fp32_cells_and_off_grid_bounds():
+    """The Shewchuk-expansion exact sums (values off the 2^-48 grid): cells of fp32 tokens are multiples of
+    2^-298 below 2^10, so any exact sum of them fits 6 non-overlapping doubles (capacity 8 is unreachable for
+    token sources); the per-cell bounds here are arbitrary float64 (off every grid). The runs read the
+    device's own float64 cells of cfg1's fp32 tokens as a matrix (a token-backed fp32 reveal sums in another
+    order than the cell kernel and can differ in the last ulp: the test above), so the traces must be
+    identical to the oracle's reveal for reveal."""
     from paper_2602_02827_b200 import BanditConfig, BanditJob, CellBounds, run_batch
     from paper_2602_02827_b200.batch import TokenBatch, exact_cells
 
     cases = [W.gen_query("cfg1", q) for q in range(3)]
     b = TokenBatch.from_host([c.query for c in cases], [case_doc_list(c) for c in cases], clamp_negative=False)
-    cells_all = exact_cells(b, with_scores=False)[0].cpu().numpy()
+    T = cases[0].query.shape[0]
+    assert all(c.query.shape[0] == T for c in cases)
+    cells_dev = exact_cells(b, with_scores=False)[0][:, :T].contiguous()
+    cells_all = cells_dev.cpu().numpy()
+    assert np.any(cells_all * 2.0**48 != np.rint(cells_all * 2.0**48)), "fp32 cells should leave the 2^-48 grid"
     rng = np.random.default_rng(7)
     jobs, refs, off = [], [], 0
     for q, c in enumerate(cases):
-        T = c.query.shape[0]
-        cells = np.ascontiguousarray(cells_all[off:off + c.n_docs, :T])
+        cells = np.ascontiguousarray(cells_all[off:off + c.n_docs])
         lo = cells - rng.uniform(1e-9, 0.6, size=cells.shape) * rng.choice([1.0, 1e-7, 1e-14], size=cells.shape)
         hi = cells + rng.uniform(1e-9, 0.6, size=cells.shape) * rng.choice([1.0, 1e-7, 1e-14], size=cells.shape)
         cfg = BanditConfig(k=5, alpha_ef=(1.0, 0.3, 0.05)[q], seed=(3, q))
         jobs.append(BanditJob(cfg, c.n_docs, T, q, off, CellBounds(lo, hi)))
         refs.append(bandit_ref.run(cells, lo, hi, 5, alpha_ef=cfg.alpha_ef, seed=(3, q)))
         off += c.n_docs
-    for got, ref in zip(run_batch(jobs, batch=b), refs):
+    for got, ref in zip(run_batch(jobs, matrix=cells_dev), refs):
         assert got.reveals == ref.reveals and got.topk == ref.topk and got.iterations == ref.iterations
 
 
