@@ -367,6 +367,18 @@ CBX_API int cbx_pcg64_draws(const cbx_pcg64* state, const uint32_t* ops, int64_t
  * row update's sub-phases setup, Welford, exact sum, interval]; NULL disables. */
 CBX_API void cbx_bandit_set_profile(void* counters);
 
+/* Row-cache variant of cbx_bandit_run (optional; reported separately from the on-demand loop):
+ * the first adaptive reveal of a row computes ALL of its cells from one gather of the document — what the
+ * reference's oracle does on first touch (oracle.py:205-215) — and later reveals of that row read them back.
+ * ``cells``: float64 [trace slots of the launch] (same offsets as the trace buffers), ``row_filled``: uint8
+ * [state rows of the launch], zeroed by the caller; both device pointers, used by the launches that follow
+ * until reset with (NULL, NULL). Token-backed runs with generic bounds only (others run on demand). Traces
+ * are identical to the on-demand loop's; cbx_bandit_out.pad returns the number of rows filled. */
+CBX_API void cbx_bandit_set_row_cache(double* cells, uint8_t* row_filled);
+/* A reveal fills its row when the row already has ``min_revealed`` cells revealed (default 2: the warm-up cell
+ * and one adaptive reveal); rows that never get that far are revealed on demand. 0 fills on first touch. */
+CBX_API void cbx_bandit_set_row_cache_threshold(int min_revealed);
+
 #ifdef __cplusplus
 }
 #endif

@@ -129,6 +129,8 @@ SIGNATURES = {
     "cbx_token_norm_max": (_I, [_P, _I64, _I, _I, _P, _P]),
     "cbx_bandit_state_bytes": (_SZ, [_I64]),
     "cbx_bandit_set_profile": (None, [_P]),
+    "cbx_bandit_set_row_cache": (None, [_P, _P]),
+    "cbx_bandit_set_row_cache_threshold": (None, [ctypes.c_int]),
     "cbx_pcg64_draws": (_I, [_P, _P, _I64, _P, _P, _P]),
     "cbx_bandit_shard_run": (_I, [_P, _P, _I64, _P, _I32, _P, _I32, _I32, _P, _I32, _P, _P, _P, _P, _SZ, _P, _I32, _P,
                                   _P, _P, _P, _P]),

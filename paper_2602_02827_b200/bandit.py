@@ -316,7 +316,8 @@ def _log_term(cfg: BanditConfig, N: int, T: int) -> float:
     return v
 
 
-def prepare_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, prewarm: bool | None = None) -> dict:
+def prepare_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, prewarm: bool | None = None,
+                  row_cache: bool | int = False) -> dict:
     """Host side of a batched launch: validate the jobs, seed the generators, build the run descriptors and
     move them (and any per-cell bounds) to the device; outputs are allocated. ``launch_batch`` then issues
     the kernels. ``prewarm`` (None = auto: when the runs fit one CTA per SM) computes the warm-up cells of
@@ -419,6 +420,14 @@ def prepare_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, prewarm: b
     tr_t = torch.empty(max(tr_off, 1), dtype=torch.int32, device=dev)
     tr_v = torch.empty(max(tr_off, 1), dtype=torch.float64, device=dev)
     out_t = torch.empty(nl * ctypes.sizeof(_lib.CbxBanditOut), dtype=torch.uint8, device=dev)
+    # row-cache variant (reported separately from the on-demand loop): float64 cells of the rows touched by
+    # adaptive reveals, same offsets as the trace buffers, plus a filled flag per state row
+    rc = None
+    if row_cache is not False and row_cache is not None and batch is not None:
+        # True: fill a row on the reveal that finds 2 of its cells already revealed; an int sets that count
+        thr = 2 if row_cache is True else int(row_cache)
+        rc = (torch.empty(max(tr_off, 1), dtype=torch.float64, device=dev),
+              torch.zeros(max(st_off, 1), dtype=torch.uint8, device=dev), thr)
     if batch is not None:
         batch.norm_max()  # the fp32 reveal screen's error bound (cbx_batch.d_norm_max), computed once per batch
     bstruct = batch.struct() if batch is not None else None
@@ -431,7 +440,7 @@ def prepare_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, prewarm: b
     return dict(results=results, live=live, descs=descs, nl=nl, max_rows=max_rows, max_k=max_k, bstruct=bstruct,
                 batch=batch, matrix=matrix, ld=ld, desc_t=desc_t, lo_t=lo_t, hi_t=hi_t, warm_t=warm_t, state=state,
                 state_bytes=state_bytes, topk=topk_t, tr_i=tr_i, tr_t=tr_t, tr_v=tr_v, out=out_t, wprefix=wprefix,
-                n_prewarm=int(sum(warm_counts)))
+                n_prewarm=int(sum(warm_counts)), row_cache=rc)
 
 
 def launch_batch(p: dict):
@@ -446,25 +455,45 @@ def launch_batch(p: dict):
             bref, p["desc_t"].data_ptr(), p["nl"], p["wprefix"].data_ptr(), p["n_prewarm"], ptr(p["warm_t"]),
             p["tr_i"].data_ptr(), p["tr_t"].data_ptr(), p["tr_v"].data_ptr(), stream), "bandit_prewarm")
     m = p["matrix"]
+    rc = p.get("row_cache")
+    if rc is not None:
+        rc[1].zero_()
+        lib.cbx_bandit_set_row_cache(rc[0].data_ptr(), rc[1].data_ptr())
+        lib.cbx_bandit_set_row_cache_threshold(rc[2])
+    try:
+        _launch_run(lib, p, m, bref, ptr, stream)
+    finally:
+        if rc is not None:
+            lib.cbx_bandit_set_row_cache(None, None)
+    return dict(descs=p["descs"], live=p["live"], topk=p["topk"], tr_i=p["tr_i"], tr_t=p["tr_t"], tr_v=p["tr_v"],
+                out=p["out"], keep=p)
+
+
+def _launch_run(lib, p, m, bref, ptr, stream):
     _lib.check(lib.cbx_bandit_run(
         bref, m.data_ptr() if m is not None else None, p["ld"], p["desc_t"].data_ptr(), p["nl"], p["max_rows"],
         ptr(p["lo_t"]), ptr(p["hi_t"]), ptr(p["warm_t"]), p["state"].data_ptr(), p["state_bytes"],
         p["topk"].data_ptr(), p["max_k"], p["tr_i"].data_ptr(), p["tr_t"].data_ptr(), p["tr_v"].data_ptr(),
         p["out"].data_ptr(), stream), "bandit_run")
-    return dict(descs=p["descs"], live=p["live"], topk=p["topk"], tr_i=p["tr_i"], tr_t=p["tr_t"], tr_v=p["tr_v"],
-                out=p["out"], keep=p)
 
 
 def run_batch(jobs: Sequence[BanditJob], batch=None, matrix=None, return_traces: bool = True, sync: bool = True,
-              prewarm: bool | None = None):
-    """Launch every job in one kernel; returns a list of RunResult (or raw device outputs if sync=False)."""
-    p = prepare_batch(jobs, batch, matrix, prewarm)
+              prewarm: bool | None = None, row_cache: bool | int = False, stats: dict | None = None):
+    """Launch every job in one kernel; returns a list of RunResult (or raw device outputs if sync=False).
+
+    ``row_cache=True`` selects the row-cache variant for token-backed runs with generic bounds: a reveal that
+    finds two cells of its row already revealed (an int sets another count; 0 = first touch) computes ALL of
+    the row's cells from one gather of the document — the reference's oracle does that on first touch,
+    oracle.py:205-215 — and later reveals of the row read them back. Results and
+    traces are identical to the on-demand loop; it gathers fewer bytes and does more arithmetic per gather,
+    so it is accounted separately (``stats["rows_filled"]``: gathers of whole rows, per run)."""
+    p = prepare_batch(jobs, batch, matrix, prewarm, row_cache)
     if not p["live"]:
         return p["results"]
     raw = launch_batch(p)
     if not sync:
         return raw
-    return collect(raw, jobs, p["results"], return_traces)
+    return collect(raw, jobs, p["results"], return_traces, stats)
 
 
 _STAGE = {}
@@ -480,7 +509,7 @@ def _pinned_stage(nbytes: int):
     return t
 
 
-def collect(raw, jobs, results=None, return_traces: bool = True):
+def collect(raw, jobs, results=None, return_traces: bool = True, stats: dict | None = None):
     """Fetch a launch's device outputs and build RunResults (raises on device-side errors)."""
     if results is None:
         results = [None] * len(jobs)
@@ -489,6 +518,9 @@ def collect(raw, jobs, results=None, return_traces: bool = True):
     live = raw["live"]
     out = np.frombuffer(raw["out"].cpu().numpy().tobytes(), dtype=np.dtype(
         [("n_reveals", "<i8"), ("iterations", "<i4"), ("terminated_by", "<i4"), ("status", "<i4"), ("pad", "<i4")]))
+    if stats is not None:
+        stats["rows_filled"] = out["pad"].astype(np.int64)  # row-cache variant: whole-row gathers per live run
+        stats["live"] = list(live)
     topk = raw["topk"].cpu().numpy()
     if return_traces:
         # only the used prefix of every run's N*T trace slots crosses PCIe: gather them on the device first

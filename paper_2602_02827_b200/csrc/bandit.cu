@@ -76,6 +76,9 @@ __global__ void pcg64_draws_kernel(cbx_pcg64 st, const uint32_t* __restrict__ op
 using namespace cbx;
 
 static unsigned long long* g_bandit_prof = nullptr;
+static double* g_bandit_cell_cache = nullptr;   // row-cache variant (cbx_bandit_set_row_cache)
+static uint8_t* g_bandit_row_filled = nullptr;
+static int g_bandit_rc_min_count = 2;
 
 static size_t state_parts(int64_t rows, size_t* off_obs, size_t* off_lo, size_t* off_hi, size_t* off_rows) {
   size_t o = 0;
@@ -109,6 +112,11 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
 extern "C" {
 
 void cbx_bandit_set_profile(void* counters) { g_bandit_prof = static_cast<unsigned long long*>(counters); }
+void cbx_bandit_set_row_cache(double* cells, uint8_t* row_filled) {
+  g_bandit_cell_cache = cells;
+  g_bandit_row_filled = row_filled;
+}
+void cbx_bandit_set_row_cache_threshold(int min_revealed) { g_bandit_rc_min_count = min_revealed < 0 ? 0 : min_revealed; }
 
 int cbx_pcg64_draws(const cbx_pcg64* state, const uint32_t* ops, int64_t n_ops, uint64_t* out, cbx_pcg64* state_out,
                     void* stream) {
@@ -310,6 +318,11 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
   P.trace_v = trace_v;
   P.out = out;
   P.prof = g_bandit_prof;
+  P.cell_cache = g_bandit_cell_cache;
+  P.row_filled = g_bandit_row_filled;
+  P.rc_smem_off = 0;
+  P.rc_cols = 0;
+  P.rc_min_count = g_bandit_rc_min_count;
   P.shard = sa ? 1 : 0;
   P.first = sa ? sa->first : 0;
   P.own_lo = sa ? sa->own_lo : 0;
@@ -369,6 +382,18 @@ static int launch_params(const cbx_batch* b, const double* matrix, int64_t ld_ma
       P.dto_smem_off = (int64_t)off;
       smem = off + need;
     }
+  }
+
+  if (P.cell_cache && b && !sa) {
+    // per-warp column front-runners of the row fill: 3 words x 16 warps x columns
+    P.rc_cols = (int32_t)((max_t + 7) / 8 * 8);
+    const size_t off = align_up(smem, 16), need = (size_t)48 * P.rc_cols * sizeof(float);
+    if (off + need > 220 * 1024) return fail(CBX_EINVAL, "bandit row cache: no shared memory left for the column table");
+    P.rc_smem_off = (int64_t)off;
+    smem = off + need;
+  } else {
+    P.cell_cache = nullptr;
+    P.row_filled = nullptr;
   }
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -127,6 +127,14 @@ struct BanditParams {
   int bounds_smem;     // expansions (+ per-cell bounds) in shared memory at byte offset bounds_smem_off
   int64_t bounds_smem_off;
   int64_t dto_smem_off;  // > 0: the run's document offsets (n_rows + 1 int64) are staged in shared memory there
+  // row-cache variant (cbx_bandit_set_row_cache; reported separately): the first adaptive reveal
+  // of a row computes all of its cells from one gather (what the reference's oracle does on first touch,
+  // oracle.py:210-215) and later reveals of the row read them back
+  double* cell_cache;    // [trace slots] float64 cells, row-major per run at the run's trace_off
+  uint8_t* row_filled;   // [state rows] 1 = the row's cells are in cell_cache
+  int64_t rc_smem_off;   // shared-memory table of per-warp column front-runners (3 x 16 warps x rc_cols words)
+  int32_t rc_cols;       // table columns (the launch's widest query rounded up to 8)
+  int32_t rc_min_count;  // cells a row must already have revealed before a reveal fills it (default 2)
   int32_t* topk;
   int32_t max_k;
   int32_t* trace_i;
@@ -1085,6 +1093,177 @@ CBX_BD_MMA_LINKAGE double tokens_max_mma(const T* __restrict__ dtok, int64_t j0,
   return best;
 }
 
+// Row-cache variant: ALL cells H[i, 0..TC) of one document from one gather. Same tensor-core screen as
+// tokens_max_mma_reload, but B carries 8 different query tokens per pass (TC / 8 passes over the staged
+// rows), so a lane reads two columns of two rows per tile off its C fragment. Each warp keeps, per column,
+// the largest and second-largest fp32 dot of its rows and the row of the largest (shared-memory table, one
+// slot per warp and column); after one barrier, column n is resolved by warp n % nwarps: every warp's
+// front-runner within 2 eps of the best is recomputed in float64 (re-read, same fma / butterfly order as
+// everywhere else), and if any warp's SECOND row could also reach the bound — or anything was not finite —
+// the column falls back to the exact single-column scan. The cells are the exact maxima either way.
+template <typename T, int KCMAX, int BT>
+__device__ __forceinline__ void row_cells_mma(const T* __restrict__ dtok, int64_t j0, int64_t j1,
+                                              const T* __restrict__ qtok, int TC, int dim, int wid, int nwarps,
+                                              int lane, double init, float xmax, float* tab, int TCP,
+                                              double* __restrict__ out_cells, int t_star,
+                                              unsigned long long* cellkey) {
+  const int nvec = dim >> 3;
+  const int kc = (nvec + 3) >> 2;
+  const int g = lane >> 2, t = lane & 3;
+  float* cmax1 = tab + (size_t)wid * TCP;
+  float* cmax2 = tab + (size_t)(16 + wid) * TCP;
+  int* crow = reinterpret_cast<int*>(tab + (size_t)(32 + wid) * TCP);
+  for (int n = lane; n < TCP; n += 32) {
+    cmax1[n] = -INFINITY;
+    cmax2[n] = -INFINITY;
+    crow[n] = -1;
+  }
+  __syncwarp();
+  const int64_t ntile = (j1 - j0 + 15) >> 4;
+  const int64_t stride = (int64_t)nwarps * BT;
+  for (int64_t tb = wid; tb < ntile; tb += stride) {  // warp-uniform
+    uint4 U[BT][KCMAX], V[BT][KCMAX];
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+      const int64_t r0 = j0 + ((tb + (int64_t)b * nwarps) << 4) + g;
+      const uint4* p0 = reinterpret_cast<const uint4*>(dtok + r0 * dim) + t;
+      const uint4* p1 = reinterpret_cast<const uint4*>(dtok + (r0 + 8) * dim) + t;
+#pragma unroll
+      for (int c = 0; c < KCMAX; ++c) {
+        U[b][c] = make_uint4(0, 0, 0, 0);
+        V[b][c] = make_uint4(0, 0, 0, 0);
+        if (c * 4 + t < nvec && r0 < j1) U[b][c] = __ldg(p0 + c * 4);
+        if (c * 4 + t < nvec && r0 + 8 < j1) V[b][c] = __ldg(p1 + c * 4);
+      }
+    }
+    for (int cb = 0; cb * 8 < TC; ++cb) {
+      // B fragment: query token cb * 8 + g in column g
+      uint4 qv[KCMAX];
+      const int qi = cb * 8 + g;
+#pragma unroll
+      for (int c = 0; c < KCMAX; ++c) {
+        qv[c] = make_uint4(0, 0, 0, 0);
+        if (qi < TC && c * 4 + t < nvec) qv[c] = __ldg(reinterpret_cast<const uint4*>(qtok + (int64_t)qi * dim) + c * 4 + t);
+      }
+      // this lane's columns 2t (k = 0) and 2t + 1 (k = 1): largest, second largest, row of the largest
+      float m1[2] = {-INFINITY, -INFINITY}, m2[2] = {-INFINITY, -INFINITY};
+      int r1[2] = {-1, -1};
+#pragma unroll
+      for (int b = 0; b < BT; ++b) {
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int c = 0; c < KCMAX; ++c) {
+          if (c < kc) {
+            mma16816<T>(acc, U[b][c].x, V[b][c].x, U[b][c].y, V[b][c].y, qv[c].x, qv[c].y);
+            mma16816<T>(acc, U[b][c].z, V[b][c].z, U[b][c].w, V[b][c].w, qv[c].z, qv[c].w);
+          }
+        }
+        const int64_t r0 = j0 + ((tb + (int64_t)b * nwarps) << 4) + g;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (r0 + 8 * h < j1) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              float sv = acc[2 * h + k];
+              if (!(fabsf(sv) <= 3.0e38f)) sv = INFINITY;  // NaN / overflow: forces the exact fallback below
+              if (sv > m1[k]) {
+                m2[k] = m1[k];
+                m1[k] = sv;
+                r1[k] = (int)(r0 + 8 * h - j0);
+              } else if (sv > m2[k]) {
+                m2[k] = sv;
+              }
+            }
+          }
+        }
+      }
+      // merge over the 8 row groups (lanes with the same t)
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const float a1 = __shfl_xor_sync(0xffffffffu, m1[k], o);
+          const float a2 = __shfl_xor_sync(0xffffffffu, m2[k], o);
+          const int ar = __shfl_xor_sync(0xffffffffu, r1[k], o);
+          if (a1 > m1[k]) {
+            m2[k] = fmaxf(m1[k], a2);
+            m1[k] = a1;
+            r1[k] = ar;
+          } else {
+            m2[k] = fmaxf(m2[k], a1);
+          }
+        }
+      }
+      if (g == 0) {  // fold into the warp's table (earlier steps of a long document)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int n = cb * 8 + 2 * t + k;
+          const float o1 = cmax1[n], o2 = cmax2[n];
+          if (m1[k] > o1) {
+            cmax1[n] = m1[k];
+            cmax2[n] = fmaxf(o1, m2[k]);
+            crow[n] = r1[k];
+          } else {
+            cmax2[n] = fmaxf(o2, m1[k]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();  // every warp's front-runners are in the table
+  const float* all1 = tab;
+  const float* all2 = tab + (size_t)16 * TCP;
+  const int* allr = reinterpret_cast<const int*>(tab + (size_t)32 * TCP);
+  for (int n = wid; n < TC; n += nwarps) {  // warp-uniform
+    const T* q = qtok + (int64_t)n * dim;
+    uint4 qw = make_uint4(0, 0, 0, 0);
+    if (lane < nvec) qw = __ldg(reinterpret_cast<const uint4*>(q) + lane);
+    float nq2 = 0.0f;
+    {
+      const T* y = reinterpret_cast<const T*>(&qw);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) nq2 = __fmaf_rn(Elem<T>::to_f(y[k]), Elem<T>::to_f(y[k]), nq2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nq2 = __fadd_rn(nq2, __shfl_xor_sync(0xffffffffu, nq2, o));
+    const bool screen = nq2 >= 0x1p-60f && nq2 <= 0x1p60f && xmax <= 0x1p60f;
+    const float qn = __fmul_ru(__fsqrt_ru(nq2), 1.0000005f);
+    const float eps = __fmaf_ru(__fmul_ru(__fmul_ru(xmax, qn), (float)dim), 0x1p-19f, 0x1p-40f);
+    const float w1 = lane < nwarps ? all1[(size_t)lane * TCP + n] : -INFINITY;
+    const float w2 = lane < nwarps ? all2[(size_t)lane * TCP + n] : -INFINITY;
+    const int wr = lane < nwarps ? allr[(size_t)lane * TCP + n] : -1;
+    float top = w1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) top = fmaxf(top, __shfl_xor_sync(0xffffffffu, top, o));
+    float LB = top == -INFINITY ? -INFINITY : __fsub_rd(top, eps);
+    if (init != -INFINITY) LB = fmaxf(LB, __double2float_rd(init));
+    // a second row of some warp could reach the bound, or a value was not finite: exact scan of the column
+    const bool amb = !screen || top == INFINITY ||
+                     __any_sync(0xffffffffu, w2 != -INFINITY && !(__fadd_ru(w2, eps) < LB));
+    double v = init;
+    if (amb) {
+      v = tokens_max_mma_reload<T, KCMAX, BT>(dtok, j0, j1, q, dim, 0, 1, lane, init, nullptr, xmax);
+    } else {
+      unsigned m = __ballot_sync(0xffffffffu, wr >= 0 && !(__fadd_ru(w1, eps) < LB));
+      while (m) {  // warp-uniform
+        const int L = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t j = j0 + __shfl_sync(0xffffffffu, wr, L);
+        double acc = 0.0;
+        if (lane < nvec) acc = vec_dot_exact<T>(__ldg(reinterpret_cast<const uint4*>(dtok + j * dim) + lane), qw);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (acc > v) v = acc;
+      }
+    }
+    if (lane == 0) {
+      out_cells[n] = v;
+      if (n == t_star) *cellkey = ord_key(v);
+    }
+  }
+}
+
 #ifndef CBX_BD_MMA_REGS
 #define CBX_BD_MMA_REGS 0
 #endif
@@ -1157,9 +1336,12 @@ __device__ __forceinline__ double tokens_max(const T* __restrict__ dtok, int64_t
 // the batch's mean document length.
 template <int NT, bool WREG>
 __host__ __device__ constexpr int bd_threads() { return NT == 512 && WREG ? 256 : NT; }
-template <typename T, int G, int VPL, int NT, bool UNI, int SM, bool WREG = false>
+// RC: the row-cache variant is compiled into its own instantiations (its code in the default kernel cost the
+// on-demand loop ~20 % through register allocation and code placement: cfg2 11.0 -> 13.5 ms, measured)
+template <typename T, int G, int VPL, int NT, bool UNI, int SM, bool WREG = false, bool RC = false>
 __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) bandit_kernel(const BanditParams P) {
   static_assert(!WREG || (NT == 512 && bd_mma_layout<T, G, VPL>()), "WREG is a wide tensor-core-screen shape");
+  static_assert(!RC || (UNI && bd_mma_layout<T, G, VPL>()), "the row cache serves generic-bounds runs on the MMA layouts");
   constexpr bool WIDE = WREG;  // rows stay in the staging registers for the exact pass
   constexpr int BD_THREADS = bd_threads<NT, WREG>();
   constexpr int BD_WARPS = BD_THREADS / 32;
@@ -1201,6 +1383,8 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
   const double* hi_b = uniform ? nullptr : P.bounds_hi + R.bounds_off;
   const bool tokens = P.q_tokens != nullptr;
   const int dim = P.dim;
+  // row-cache variant: token-backed runs with generic bounds on the tensor-core screen's layouts
+  const bool rcache = RC && P.cell_cache != nullptr && tokens && !P.shard;
 
   struct Ctrl {
     int action;       // 0 reveal, 1 stop, 2 warm-up, 3 exhaustion, 4 error
@@ -1212,6 +1396,8 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
     unsigned long long cellkey;
     int32_t swap_in, swap_out;  // best non-member / worst member of the last selection
     int32_t partner;            // row whose membership swapped with i* this iteration (-1: none)
+    int32_t hit;                // row-cache variant: the cell of this iteration came from the cache
+    int32_t fills;              // row-cache variant: rows whose cells were computed (one gather each)
     int64_t j0, j1;             // token range of i* (read by the decision with its other loads)
   };
   static_assert(sizeof(Ctrl) <= 128, "control block");
@@ -1405,6 +1591,8 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
     ctrl->status = resume ? step->status : 0;
     ctrl->n_reveals = resume ? step->n_reveals : 0;
     ctrl->iterations = resume ? step->iterations : 0;
+    ctrl->fills = 0;
+    ctrl->hit = 0;
     if (resume) {
       ctrl->i_star = step->i_star;
       ctrl->t_star = step->t_star;
@@ -1605,6 +1793,17 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
             ctrl->t_star = t_star;
             ctrl->cellkey = ord_key(init_cell);
             ctrl->lbkey = 0u;
+            if constexpr (RC) {
+              if (rcache) {
+                // both loads at once; the cached value only counts when the row has been filled. A row is
+                // filled on the reveal that finds rc_min_count cells of it already revealed: rows that never
+                // get that far (most of a pool: the warm-up cell plus one adaptive reveal) stay on demand
+                const uint8_t f = P.row_filled[R.state_off + i_star];
+                const double cv = P.cell_cache[R.trace_off + (int64_t)i_star * TC + t_star];
+                ctrl->hit = f ? 1 : (TC - un.count() >= P.rc_min_count ? 0 : 2);  // 2: on demand, no fill
+                if (f) ctrl->cellkey = ord_key(cv);
+              }
+            }
 #if CBX_BD_DOC_PREFETCH
             if (tokens) {
               const int64_t j0 = i_star == i_plus ? jp0 : jm0, j1 = i_star == i_plus ? jp1 : jm1;
@@ -1612,7 +1811,7 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
               ctrl->j1 = j1;
               // start streaming the document into L2 now; the reveal's loads then meet it on the way
               const uint32_t nb = (uint32_t)((j1 - j0) * (int64_t)dim * (int64_t)sizeof(T));
-              if (nb >= 16 && (!P.shard || (i_star >= own_lo && i_star < own_hi)))
+              if (nb >= 16 && (!P.shard || (i_star >= own_lo && i_star < own_hi)) && !(RC && rcache && ctrl->hit == 1))
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(dtok + j0 * dim), "r"(nb) : "memory");
 #if CBX_BD_DOC_PREFETCH >= 2
               // the other boundary row is often the next one revealed: warm it as well
@@ -1742,7 +1941,24 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
     i_star = ctrl->i_star;
     t_star = ctrl->t_star;
     const bool own = !P.shard || (i_star >= own_lo && i_star < own_hi);
-    if (tokens && own) {
+    const int rc_mode = (RC && rcache) ? ctrl->hit : 2;  // 0 fill the row, 1 served from the cache, 2 on demand
+    if (RC && rc_mode != 2) {
+      static_assert(CBX_BD_DOC_PREFETCH, "the row fill takes the token range from the decision");
+      if constexpr (RC) {
+        if (rc_mode == 0) {  // CTA-uniform: all of the row's cells from one gather
+          constexpr int KCMAX = (G * VPL) / 4;
+          row_cells_mma<T, KCMAX, (KCMAX <= 4 ? 2 : 1)>(
+              dtok, ctrl->j0, ctrl->j1, qtok, TC, dim, warp, BD_WARPS, lane, init_cell, P.xmax,
+              reinterpret_cast<float*>(bd_smem + P.rc_smem_off), P.rc_cols,
+              P.cell_cache + R.trace_off + (int64_t)i_star * TC, t_star, &ctrl->cellkey);
+          __syncthreads();
+          if (tid == 0) {
+            P.row_filled[R.state_off + i_star] = 1;
+            ctrl->fills += 1;
+          }
+        }
+      }
+    } else if (tokens && own) {
 #if CBX_BD_DOC_PREFETCH
       const int64_t j0 = ctrl->j0, j1 = ctrl->j1;
 #else
@@ -1912,7 +2128,7 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
     o.iterations = ctrl->iterations;
     o.terminated_by = term;
     o.status = ctrl->status;
-    o.pad = 0;
+    o.pad = ctrl->fills;  // row-cache variant: rows filled (0 otherwise)
     P.out[blockIdx.x] = o;
     if (P.shard && !P.mbox) {
       step->phase = CBX_SHARD_DONE;
@@ -1965,6 +2181,22 @@ __global__ void __launch_bounds__(256) warm_cells_kernel(const BanditParams P, i
 #ifndef CBX_BD_WREG_MAX_MEAN_ROWS
 #define CBX_BD_WREG_MAX_MEAN_ROWS 320  // wide launches: the 256-thread register shape up to this mean document length
 #endif
+template <typename T, int G, int VPL>
+static void (*pick_bandit_rc(bool wide, int sm, bool wreg))(const BanditParams) {
+  if constexpr (bd_mma_layout<T, G, VPL>()) {
+    if constexpr (G * VPL <= 16) {
+      if (wide && wreg)
+        return sm == 2 ? bandit_kernel<T, G, VPL, 512, true, 2, true, true>
+                       : (sm == 1 ? bandit_kernel<T, G, VPL, 512, true, 1, true, true>
+                                  : bandit_kernel<T, G, VPL, 512, true, 0, true, true>);
+    }
+    if (wide) return sm == 2 ? bandit_kernel<T, G, VPL, 512, true, 2, false, true>
+                             : (sm == 1 ? bandit_kernel<T, G, VPL, 512, true, 1, false, true>
+                                        : bandit_kernel<T, G, VPL, 512, true, 0, false, true>);
+    return sm == 2 ? bandit_kernel<T, G, VPL, 256, true, 2, false, true> : bandit_kernel<T, G, VPL, 256, true, 0, false, true>;
+  }
+  return nullptr;
+}
 template <typename T, int G, int VPL, bool UNI>
 static void (*pick_bandit(bool wide, int sm, bool wreg))(const BanditParams) {
   if constexpr (bd_mma_layout<T, G, VPL>() && G * VPL <= 16) {
@@ -1990,6 +2222,10 @@ static int launch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, cud
   auto kern = pick_bandit<T, G, VPL, false>(wide, sm, wreg);
   if constexpr (sizeof(T) == 2) {  // the BASELINE configs: 16-bit tokens with generic bounds
     if (P.bounds_lo == nullptr) kern = pick_bandit<T, G, VPL, true>(wide, sm, wreg);
+    if (P.bounds_lo == nullptr && P.cell_cache != nullptr && !P.shard) {  // row-cache variant
+      auto k2 = pick_bandit_rc<T, G, VPL>(wide, sm, wreg);
+      if (k2) kern = k2;
+    }
   }
   CBX_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (P.mbox && n_runs > 1) {

@@ -99,8 +99,10 @@ def test_token_backed_runs_match_reference_trace_for_trace():
 
 @pytest.mark.parametrize("name,q", [("cfg1", 0), ("cfg2", 0), ("cfg2", 1), ("cfg2", 2), ("cfg3", 0), ("cfg3", 1),
                                     ("cfg5", 0), ("cfg5", 1)])
-def test_config_query_bandit_matches_reference(name, q):
-    """Full-shape queries of each BASELINE config (seed (0, q)); cfg5 sweeps all five alphas."""
+@pytest.mark.parametrize("row_cache", [False, True, 0])
+def test_config_query_bandit_matches_reference(name, q, row_cache):
+    """Full-shape queries of each BASELINE config (seed (0, q)); cfg5 sweeps all five alphas. ``row_cache``:
+    the variant that computes all cells of a row on its first adaptive reveal must give the same traces."""
     from paper_2602_02827_b200 import BanditConfig, BanditJob, run_batch
     from helpers import batch_of_cases
 
@@ -114,7 +116,13 @@ def test_config_query_bandit_matches_reference(name, q):
     lq = case.query.shape[0]
     jobs = [BanditJob(BanditConfig(k=cfg.k, alpha_ef=a, seed=(0, q)), case.n_docs, lq, 0, 0, (-1.0, 1.0))
             for a in cfg.alphas]
-    results = run_batch(jobs, batch=b)
+    stats = {}
+    results = run_batch(jobs, batch=b, row_cache=row_cache, stats=stats)
+    # row_cache: True = fill a row once it has two revealed cells, 0 = fill on first touch
+    if row_cache is not False and cfg.dtype != "f32":  # fp32 tokens run on demand (no tensor-core screen)
+        assert 0 < int(stats["rows_filled"].max()) <= case.n_docs
+    else:
+        assert int(stats["rows_filled"].sum()) == 0
     for ai, res in enumerate(results):
         exp_it = z[f"a{ai}_trace_it"]
         got_it = np.array([(i, t) for i, t, _ in res.reveals], dtype=np.int32).reshape(-1, 2)
@@ -432,3 +440,51 @@ def test_expansion_capacity_overflow_raises_instead_of_returning_a_wrong_sum():
         assert "expansion" in str(e) or "exact" in str(e), e
     else:
         assert got.reveals == ref.reveals and got.topk == ref.topk
+
+
+def test_row_cache_variant_on_ragged_clamped_and_long_documents():
+    """Row-cache variant against the on-demand loop and the oracle: 1-token to 1100-token documents (several
+    reveal steps per document), clamp_negative, bf16, queries of 5 / 37 / 100 tokens (column blocks of 8 with
+    a ragged tail), duplicated tokens (exact ties between rows: the ambiguous-column fallback)."""
+    from paper_2602_02827_b200 import BanditConfig, BanditJob, run_batch
+    from paper_2602_02827_b200.batch import TokenBatch, to_torch_tokens
+
+    rng = np.random.default_rng(4242)
+    d = 128
+    qs, docs_q, cells_q = [], [], []
+    for lq in (5, 37, 100):
+        qv = rng.standard_normal((lq, d))
+        qv /= np.linalg.norm(qv, axis=1, keepdims=True)
+        lens = np.concatenate([[1, 2, 15, 16, 17, 255, 256, 257, 1100], rng.integers(1, 300, size=40)])
+        docs = []
+        for L in lens:
+            x = rng.standard_normal((int(L), d))
+            x /= np.linalg.norm(x, axis=1, keepdims=True)
+            if L >= 4:
+                x[L // 2] = x[0]  # an exact tie inside the document
+            docs.append(x)
+        docs[3] = docs[4][:16].copy()  # two documents sharing their best rows
+        qb = W.bf16_bits_from_f32(qv.astype(np.float32))
+        db = [W.bf16_bits_from_f32(x.astype(np.float32)) for x in docs]
+        qs.append(qb)
+        docs_q.append(db)
+        cells = maxsim_ref.cell_matrix(W.to_float64(qb, "bf16"), [W.to_float64(x, "bf16") for x in db])
+        cells_q.append(np.maximum(cells, 0.0))
+    b = TokenBatch.from_host([to_torch_tokens(q, "bf16") for q in qs],
+                             [[to_torch_tokens(x, "bf16") for x in db] for db in docs_q], clamp_negative=True)
+    jobs, refs, off = [], [], 0
+    for qi, (qb, db) in enumerate(zip(qs, docs_q)):
+        for a in (1.0, 0.1):
+            cfg = BanditConfig(k=4, alpha_ef=a, seed=(9, qi))
+            jobs.append(BanditJob(cfg, len(db), qb.shape[0], qi, off, (0.0, 1.0)))
+            refs.append(bandit_ref.run(cells_q[qi], 0.0, 1.0, 4, alpha_ef=a, seed=(9, qi)))
+        off += len(db)
+    stats = {}
+    plain = run_batch(jobs, batch=b)
+    cached = run_batch(jobs, batch=b, row_cache=True, stats=stats)
+    first = run_batch(jobs, batch=b, row_cache=0)  # fill on first touch
+    assert int(stats["rows_filled"].max()) > 0
+    for g, c, f, r in zip(plain, cached, first, refs):
+        assert g.reveals == r.reveals and g.topk == r.topk
+        assert c.reveals == r.reveals and c.topk == r.topk and c.iterations == r.iterations
+        assert f.reveals == r.reveals and f.topk == r.topk

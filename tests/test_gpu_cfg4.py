@@ -116,12 +116,14 @@ def _assert_trace(res, z):
     assert res.terminated_by == ("separation" if sep else "exhaustion")
 
 
-def test_p2_single_gpu_trace(cfg4):
+@pytest.mark.parametrize("row_cache", [False, True])
+def test_p2_single_gpu_trace(cfg4, row_cache):
     from paper_2602_02827_b200 import BanditConfig, BanditJob, run_batch
 
     case, b, z = cfg4
     cfg = W.CONFIGS["cfg4"]
-    res = run_batch([BanditJob(BanditConfig(k=cfg.k, seed=(0, 0)), case.n_docs, 32, 0, 0, (-1.0, 1.0))], batch=b)[0]
+    res = run_batch([BanditJob(BanditConfig(k=cfg.k, seed=(0, 0)), case.n_docs, 32, 0, 0, (-1.0, 1.0))], batch=b,
+                    row_cache=row_cache)[0]
     _assert_trace(res, z)
 
 

@@ -21,6 +21,8 @@ ap.add_argument("--phases", action="store_true")
 ap.add_argument("--selection", default="auto")
 ap.add_argument("--no-prewarm", action="store_true")
 ap.add_argument("--prewarm", action="store_true")
+ap.add_argument("--row-cache", type=int, default=None, nargs="?", const=2,
+                help="the row-cache variant; value = cells a row must have revealed before a reveal fills it")
 ap.add_argument("--runs", type=int, default=None, help="runs over the first --queries queries, round robin (footprint test)")
 a = ap.parse_args()
 cfg = W.CONFIGS[a.config]
@@ -42,7 +44,8 @@ if a.phases:
 elem = b.d_tokens.element_size()
 for it in range(a.iters):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    prep = prepare_batch(jobs, batch=b, prewarm=False if a.no_prewarm else (True if a.prewarm else None))
+    prep = prepare_batch(jobs, batch=b, prewarm=False if a.no_prewarm else (True if a.prewarm else None),
+                         row_cache=False if a.row_cache is None else int(a.row_cache))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e0.record()
@@ -51,7 +54,8 @@ for it in range(a.iters):
     torch.cuda.synchronize()
     host = time.perf_counter() - t0
     ms = e0.elapsed_time(e1)
-    res = collect(raw, jobs, list(prep["results"]))
+    st = {}
+    res = collect(raw, jobs, list(prep["results"]), stats=st)
     reveals = sum(len(r.reveals) for r in res)
     iters = sum(r.iterations for r in res)
     gbytes = 0
@@ -63,7 +67,8 @@ for it in range(a.iters):
     print(f"iter {it}: {len(jobs)} runs, kernel {ms:.2f} ms (host {host*1e3:.1f} ms), reveals {reveals}, "
           f"iterations {iters}, {reveals / ms * 1e3 / 1e6:.2f} M cells/s, gather {gbytes / ms / 1e6:.0f} GB/s, "
           f"coverage mean {cov.mean():.4f} [{cov.min():.4f}, {cov.max():.4f}], "
-          f"{iters / ms * 1e3 / 1e6:.3f} M iter/s aggregate")
+          f"{iters / ms * 1e3 / 1e6:.3f} M iter/s aggregate"
+          + (f", rows filled {int(st['rows_filled'].sum())}" if a.row_cache is not None else ""))
     if prof is not None:
         ph = prof.view(-1, 16).cpu().numpy().astype(np.float64)
         its = np.array([r.iterations for r in res], dtype=np.float64)
