@@ -337,8 +337,8 @@ def run_ours(args, rank, world, local_rank):
                              "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(nq_all * K * 8),
                              "ms_per_step": e_ms,
                              "api": "batch.Corpus.rerank_topk: corpus resident in HBM (fit once, untimed); per step "
-                                    "H2D query tokens + candidate ids, TMA streams candidates straight from the "
-                                    "corpus (32-row packed layout), score, Top-K, D2H Top-K; "
+                                    "H2D query tokens + candidate ids, maxsim_docs_kernel scores the candidates in "
+                                    "place in the corpus (document tiles by TMA, tcgen05), Top-K, D2H Top-K; "
                                     "max of device-event and host wall time, max over ranks",
                              "topk_equals_device_path": bool(got_docs is not None and
                                                              np.array_equal(got_docs, ref_docs))}

@@ -532,8 +532,10 @@ def collect(raw, jobs, results=None, return_traces: bool = True, stats: dict | N
         total = int(cum[-1])
         if total:
             # one device gather of the used slots, two D2H copies into pinned memory, one synchronisation
-            shift = torch.from_numpy(np.repeat(starts - cum[:-1], nrev)).pin_memory().to(dev, non_blocking=True)
-            pos = torch.arange(total, dtype=torch.int64, device=dev) + shift
+            # slot -> trace position: per-run shifts expanded on the device (a few hundred values cross PCIe)
+            small = torch.from_numpy(np.stack([starts - cum[:-1], nrev])).to(dev)
+            pos = torch.arange(total, dtype=torch.int64, device=dev) + \
+                torch.repeat_interleave(small[0], small[1], output_size=total)
             blk = torch.empty((total, 4), dtype=torch.int32, device=dev)  # (i, t, v lo word, v hi word)
             blk[:, 0] = raw["tr_i"][pos]
             blk[:, 1] = raw["tr_t"][pos]
