@@ -1494,22 +1494,43 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
 
   // ledger._record (oracle.py:305-314) + refresh(i) (bandit.py:220-247) for one row
   // pre: the two unrevealed-bound sums after removing column t, already computed (per-cell bounds)
+  double last_proxy = 0.0;  // proxy written by the last reveal_update of this thread (saves re-reading it)
   auto reveal_update = [&](int i, int t, double v, bool have_pre = false, double pre_lo = 0.0,
                            double pre_hi = 0.0) -> bool {
+    // every load of the row up front, in one batch: with the rows in global memory (pools above BD_SMEM_ROWS)
+    // each read-modify-write below would otherwise stall the thread for its own L2 round trip
     const int n = rv.cnt[i] + 1;
     double mean = rv.mean[i], m2 = rv.m2[i];
+    const uint8_t em = rv.exp_mode[i];
+    long long fx = rv.fx[i];
+    const uint64_t ulo = rv.unrev_lo[i], uhi = rv.unrev_hi[i];
     BD_PHASE(8);
     const double d = __dsub_rn(v, mean);
     mean = __dadd_rn(mean, __ddiv_rn(d, (double)n));
     m2 = __dadd_rn(m2, __dmul_rn(d, __dsub_rn(v, mean)));
     BD_PHASE(9);
-    bool ok = obs_add(i, v);
-    const double obs = obs_sum(i);
+    // the row's exact sum (math.fsum of its revealed values): int64 fixed point on the 2^-48 grid, else an expansion
+    bool ok = true;
+    double obs;
+    long long q;
+    if (__builtin_expect(!em, 1)) {
+      if (__builtin_expect(to_fixed(v, q), 1)) {
+        fx += q;
+        rv.fx[i] = fx;
+        obs = __dmul_rn(__ll2double_rn(fx), BD_FX_INV);
+      } else {  // leave the grid: the int64 sum becomes an exact two-term expansion
+        rv.exp_mode[i] = 1;
+        ok = exp_leave_grid(&g_obs[i], fx, v);
+        obs = exp_value(&g_obs[i]);
+      }
+    } else {
+      ok = exp_add(&g_obs[i], v, &obs);
+    }
     BD_PHASE(10);
     rv.mean[i] = mean;
     rv.m2[i] = m2;
-    if (t < 64) rv.unrev_lo[i] &= ~(1ull << t);
-    else rv.unrev_hi[i] &= ~(1ull << (t - 64));
+    if (t < 64) rv.unrev_lo[i] = ulo & ~(1ull << t);
+    else rv.unrev_hi[i] = uhi & ~(1ull << (t - 64));
     rv.cnt[i] = n;
     double lo_sum, hi_sum;
     if (uniform) {
@@ -1528,6 +1549,7 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
     rv.proxy[i] = px;
     rv.lcb[i] = l;
     rv.ucb[i] = u;
+    last_proxy = px;
     BD_PHASE(11);
     return ok;
   };
@@ -2049,13 +2071,17 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
     if (tid == 0) {
       const double v = (tokens || P.shard) ? ord_val(ctrl->cellkey)
                                            : P.matrix[(R.row_begin + i_star) * P.ld_matrix + t_star];
+      // what the membership test below reads of OTHER rows, loaded with the row's own state (one round trip)
+      const int sw_in = ctrl->swap_in, sw_out = ctrl->swap_out;
+      const uint8_t was_member = rv.member[i_star];
+      const double p_in = sw_in >= 0 ? rv.proxy[sw_in] : 0.0, p_out = sw_out >= 0 ? rv.proxy[sw_out] : 0.0;
       if (!reveal_update(i_star, t_star, v, !uniform, pre_lo, pre_hi)) ctrl->status = 2;
       // keep the Top-K set equal to the first K of the (-proxy, i) order
-      const uint64_t mk = ord_key(rv.proxy[i_star]);
-      if (rv.member[i_star]) {
-        const int b = ctrl->swap_in;  // best non-member
+      const uint64_t mk = ord_key(last_proxy);
+      if (was_member) {
+        const int b = sw_in;  // best non-member
         if (b >= 0) {
-          const uint64_t bk = ord_key(rv.proxy[b]);
+          const uint64_t bk = ord_key(p_in);
           if (bk > mk || (bk == mk && b < i_star)) {
             rv.member[i_star] = 0;
             rv.member[b] = 1;
@@ -2063,9 +2089,9 @@ __global__ void __launch_bounds__(bd_threads<NT, WREG>(), NT == 256 ? 2 : 1) ban
           }
         }
       } else {
-        const int w = ctrl->swap_out;  // worst member
+        const int w = sw_out;  // worst member
         if (w >= 0) {
-          const uint64_t wk = ord_key(rv.proxy[w]);
+          const uint64_t wk = ord_key(p_out);
           if (mk > wk || (mk == wk && i_star < w)) {
             rv.member[i_star] = 1;
             rv.member[w] = 0;
