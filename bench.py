@@ -754,9 +754,18 @@ def run_stage1(args, rank, world):
         toks = corpus.tokens[: int(do[n_docs])].double().cpu().numpy()
         docs = [toks[do[i]:do[i + 1]] for i in range(n_docs)]
         t0 = time.perf_counter()
-        stage1_ref.generate_candidates(q64, docs, kp, True)
+        _, _, ref_nb = stage1_ref.generate_candidates(q64, docs, kp, True)
         cpu_s = time.perf_counter() - t0
         del lim
+        # the device scan (tcgen05 filter + float64 refine) over the same sub-corpus against the CPU oracle's
+        # neighbour lists: global token index and float64 similarity, token for token
+        sub = Corpus(corpus.tokens[: int(do[n_docs])], do[: n_docs + 1].copy(), clamp_negative=True)
+        tk_s, vl_s = stage1_topk(sub, q, kp, True, path="tc")
+        ref_tok = np.array([[int(do[d]) + j for d, j, _ in nbs] for nbs in ref_nb], dtype=np.int64)
+        ref_val = np.array([[v for *_, v in nbs] for nbs in ref_nb], dtype=np.float64)
+        out["parity"]["tc_equals_cpu_oracle"] = bool(np.array_equal(tk_s, ref_tok) and np.array_equal(vl_s, ref_val))
+        out["parity"]["cpu_oracle_sample"] = f"first {n_docs} cfg4 docs ({int(do[n_docs])} tokens), path " + \
+            "/".join(sorted(set(stage1_topk.last_paths)))
         out["cpu_baseline"] = {"value": R * int(do[n_docs]) / cpu_s, "unit": "similarities/s", "cores": 1,
                                "kind": "port", "sample": f"oracle/stage1_ref.generate_candidates over the first "
                                                          f"{n_docs} cfg4 docs ({int(do[n_docs])} tokens), {cpu_s:.1f} s"}

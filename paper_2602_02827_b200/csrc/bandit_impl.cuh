@@ -315,17 +315,21 @@ __device__ __forceinline__ void tree_leaf(const Trees& t, const RowsView& rv, in
                                           unsigned mask = 0xFu) {
   const int i = g * 32 + lane;
   const bool live = i < N;
-  const bool mem = live && rv.member[i];
+  // the membership flag and the selection's value are loaded together, not one after the other: with the
+  // rows in global memory (pools above BD_SMEM_ROWS) a dependent pair costs two L2 round trips per refresh
+  const uint8_t memb = live ? rv.member[i] : 0;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     if (!(mask >> s & 1u)) continue;
+    double val = 0.0;
+    if (live) val = s == 0 ? rv.lcb[i] : (s == 1 ? rv.ucb[i] : rv.proxy[i]);
+    const bool mem = memb != 0;
     // selections 0 and 3 range over members, 1 and 2 over non-members (no indexed local array)
     Cand c{0, TIE_EMPTY};
     if (live && (mem == (s == 0 || s == 3))) {
-      if (s == 0) c = Cand{~ord_key(rv.lcb[i]), (uint32_t)i};
-      else if (s == 1) c = Cand{ord_key(rv.ucb[i]), (uint32_t)i};
-      else if (s == 2) c = Cand{ord_key(rv.proxy[i]), (uint32_t)i};
-      else c = Cand{~ord_key(rv.proxy[i]), ~(uint32_t)i};
+      if (s == 0) c = Cand{~ord_key(val), (uint32_t)i};
+      else if (s == 1 || s == 2) c = Cand{ord_key(val), (uint32_t)i};
+      else c = Cand{~ord_key(val), ~(uint32_t)i};
     }
     const Cand w = warp_best(c);
     if (lane == 0) {
