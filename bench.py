@@ -374,11 +374,27 @@ def run_ours(args, rank, world, local_rank):
                 result[name] = {"skipped": f"time budget of {args.budget_s:.0f} s used up by the earlier sections"}
             return
         _log(f"section {name}: start")
+        # multi-rank sections exchange data between ranks inside kernels and collectives: if a peer is lost, a
+        # rank can wait forever. A watchdog then prints the line with what is already measured and ends the rank.
+        timer = None
+        if world > 1:
+            def _bail():
+                if rank == 0:
+                    result[name] = {"error": f"watchdog: section did not finish within {args.section_timeout_s:.0f} s"}
+                    print(json.dumps(result), flush=True)
+                os._exit(0)
+
+            timer = threading.Timer(args.section_timeout_s, _bail)
+            timer.daemon = True
+            timer.start()
         try:
             out = fn()
         except Exception as e:  # noqa: BLE001
             out = {"error": f"{type(e).__name__}: {e}"[:500]}
             print(f"bench: section {name} failed: {out['error']}", file=sys.stderr, flush=True)
+        finally:
+            if timer is not None:
+                timer.cancel()
         _log(f"section {name}: done")
         if rank == 0:
             result[name] = out
@@ -1110,6 +1126,9 @@ def main():
     ap.add_argument("--no-p2-sharded", action="store_true")
     ap.add_argument("--no-p2-host-stepped", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="launcher/sharding/reduction only, no GPU (gloo)")
+    ap.add_argument("--section-timeout-s", type=float, default=240.0,
+                    help="multi-rank runs: a section beside the headline that takes longer ends the run with the "
+                         "line measured so far")
     ap.add_argument("--budget-s", type=float, default=420.0,
                     help="sections beside the headline start only while the run is younger than this (seconds)")
     args = ap.parse_args()
