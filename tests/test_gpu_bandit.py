@@ -474,10 +474,10 @@ def test_row_cache_variant_on_ragged_clamped_and_long_documents():
                              [[to_torch_tokens(x, "bf16") for x in db] for db in docs_q], clamp_negative=True)
     jobs, refs, off = [], [], 0
     for qi, (qb, db) in enumerate(zip(qs, docs_q)):
-        for a in (1.0, 0.1):
-            cfg = BanditConfig(k=4, alpha_ef=a, seed=(9, qi))
-            jobs.append(BanditJob(cfg, len(db), qb.shape[0], qi, off, (0.0, 1.0)))
-            refs.append(bandit_ref.run(cells_q[qi], 0.0, 1.0, 4, alpha_ef=a, seed=(9, qi)))
+        for a, mode in ((1.0, "epsilon-greedy"), (0.1, "epsilon-greedy"), (0.3, "static-warmup"), (0.3, "uniform-row")):
+            kw = dict(alpha_ef=a, explore_mode=mode, gamma_init=0.15 if mode == "static-warmup" else 0.0, seed=(9, qi))
+            jobs.append(BanditJob(BanditConfig(k=4, **kw), len(db), qb.shape[0], qi, off, (0.0, 1.0)))
+            refs.append(bandit_ref.run(cells_q[qi], 0.0, 1.0, 4, **kw))
         off += len(db)
     stats = {}
     plain = run_batch(jobs, batch=b)
