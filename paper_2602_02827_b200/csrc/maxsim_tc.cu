@@ -36,8 +36,12 @@ namespace cbx {
 constexpr int TC_THREADS = (CBX_TC_EPI_WARP0 + 4) * 32;
 constexpr int TC_EPI_WARP0 = CBX_TC_EPI_WARP0;
 static_assert(TC_EPI_WARP0 % 4 == 0, "epilogue warps must cover TMEM lane quarters 0..3 in order");
-constexpr int TC_ACC_BUFS = 4;
-constexpr int TC_MAX_TILE_N = 128;
+constexpr int TC_ACC_BUFS = 4;      // accumulator barrier pairs (a ring of four, whatever the number of accumulators)
+constexpr int TC_TMEM_COLS = 512;   // all of TMEM: 4 accumulators of 128 columns, or 2 of 256
+constexpr int TC_MAX_TILE_N = 256;
+#ifndef CBX_TC_TILE256
+#define CBX_TC_TILE256 1  // contiguous batches with d <= 128: 256-token tiles (half the per-tile work per byte)
+#endif
 #ifndef CBX_PK_TILE_N
 #define CBX_PK_TILE_N 128  // packed-mode tile height (build knob; 64 measured much slower)
 #endif
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int k = 0; k < 5; ++k) ptx::prefetch_tmap(&tm.d[k]);
     ptx::prefetch_tmap(&tm.q);
   }
-  if (warp == 1) ptx::tmem_alloc<TC_ACC_BUFS * TC_MAX_TILE_N>(tmem_holder);
+  if (warp == 1) ptx::tmem_alloc<TC_TMEM_COLS>(tmem_holder);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -352,12 +356,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         qphase ^= 1;
         ptx::tc_fence_after();
         for (int t = 0; t < c.ntiles; ++t, ++tg) {
-          const uint32_t acc = tg & (TC_ACC_BUFS - 1);
-          ptx::mbar_wait(&tempty[acc], ((tg >> 2) & 1) ^ 1);
+          // accumulators: 4 x 128 columns, or 2 x 256 for 256-token tiles; their barriers are a ring of four
+          // indexed by the tile either way (a group of the epilogue meets every rep-th tile: a barrier shared
+          // with another group's tiles would put its waiter two phases behind — parity aliasing)
+          const uint32_t nacc = p.tile_n > 128 ? 2u : 4u;
+          const uint32_t acc = tg & (nacc - 1);
+          if (tg >= nacc) ptx::mbar_wait(&tempty[(tg - nacc) & 3], ((tg - nacc) >> 2) & 1);
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t b_addr = ptx::smem_u32(stages + (size_t)stage * p.stage_bytes);
-          const uint32_t d_tmem = tmem_base + acc * TC_MAX_TILE_N;
+          const uint32_t d_tmem = tmem_base + acc * (p.tile_n > 128 ? 256u : 128u);
           // descriptors advance by (byte offset >> 4) in their 14-bit start-address field
           // interleaved (packed) stages: K block kb is 1 KB into each 8-row group, groups kblocks KB apart
           const uint64_t bd0 = ptx::smem_desc_sw128(b_addr, p.ilv ? (uint32_t)p.kblocks * 1024u : 1024u);
@@ -371,7 +379,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                               p.idesc, (kb | k4) != 0);
           }
           ptx::tc_commit(&empty[stage]);
-          ptx::tc_commit(&tfull[acc]);
+          ptx::tc_commit(&tfull[tg & 3]);
           if (++stage == (uint32_t)p.stages) { stage = 0; phase ^= 1; }
         }
         ptx::tc_commit(qempty);
@@ -411,20 +419,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         int64_t prev_end = c.cs;
         for (int t = 0; t < c.ntiles; ++t, ++tg) {
           if ((int)(tg % (uint32_t)rep) != grp) continue;
-          const uint32_t acc = tg & (TC_ACC_BUFS - 1);
-          ptx::mbar_wait(&tfull[acc], (tg >> 2) & 1);
+          const uint32_t acc = tg & (p.tile_n > 128 ? 1u : 3u);
+          ptx::mbar_wait(&tfull[tg & 3], (tg >> 2) & 1);
           ptx::tc_fence_after();
           const int64_t tb = c.cs + (int64_t)t * p.tile_n;
           const int ncols = (int)(c.ce - tb < p.tile_n ? c.ce - tb : p.tile_n);
-          float v[TC_MAX_TILE_N / 32][32];
-          const uint32_t taddr = tmem_base + tmem_lane + acc * TC_MAX_TILE_N;
+          // the accumulator is read 128 columns at a time (the registers' worth); `vload(hf)` brings half hf
+          float v[4][32];
+          const uint32_t taddr = tmem_base + tmem_lane + acc * (p.tile_n > 128 ? 256u : 128u);
+          auto vload = [&](int hf) {
 #pragma unroll
-          for (int b = 0; b < TC_MAX_TILE_N / 32; ++b)
-            if (b * 32 < ncols) ptx::tmem_ld_32x32b_x32(taddr + b * 32, v[b]);
-          ptx::tmem_ld_wait();
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            for (int b = 0; b < 4; ++b)
+              if (hf * 128 + b * 32 < ncols) ptx::tmem_ld_32x32b_x32(taddr + hf * 128 + b * 32, v[b]);
+            ptx::tmem_ld_wait();
+            if ((hf + 1) * 128 >= ncols) {  // the last columns are out: hand the accumulator back
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(&tempty[tg & 3]);
+            }
+          };
+          vload(0);
 
           // skip documents that ended before this tile (other groups' tiles)
           int64_t cur_end;
@@ -478,11 +492,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             cur_end = __shfl_sync(0xffffffffu, ends, (int)(doc - win));
           };
+          for (int hf = 0; hf * 128 < ncols; ++hf) {
+          if (hf > 0) vload(hf);
 #pragma unroll
-          for (int b = 0; b < TC_MAX_TILE_N / 32; ++b) {
-            if (b * 32 >= ncols) break;
-            const int64_t g0 = tb + b * 32;  // stream row of this block's column 0
-            const int nc = ncols - b * 32 < 32 ? ncols - b * 32 : 32;
+          for (int b = 0; b < 4; ++b) {
+            if (hf * 128 + b * 32 >= ncols) break;
+            const int64_t g0 = tb + hf * 128 + b * 32;  // stream row of this block's column 0
+            const int nc = ncols - hf * 128 - b * 32 < 32 ? ncols - hf * 128 - b * 32 : 32;
             while (true) {
               const int64_t ds = doc_start - g0;
               if (ds >= nc) break;  // the current document starts after this block (packed padding)
@@ -494,6 +510,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               if (de > nc) break;  // document continues past this block
               close_seg();
             }
+          }
           }
           // carry chain: merge the previous tile's open document into this head
           float p_prev = init;
@@ -533,7 +550,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<TC_ACC_BUFS * TC_MAX_TILE_N>(tmem_base);
+    ptx::tmem_dealloc<TC_TMEM_COLS>(tmem_base);
   }
 }
 
@@ -1004,9 +1021,10 @@ struct TcLaunch {
 };
 
 static int prepare_tc(const cbx_batch* b, const void* d_rows, int64_t n_rows, float* scores, TcLaunch& L,
-                      int tile_cap = 128) {
+                      int tile_cap = CBX_TC_TILE256 ? 256 : 128) {
   const int kblocks = (b->dim + 63) / 64;
-  int tile_n = kblocks <= 4 ? 128 : 32;  // d <= 256: N=128 MMAs; d=512: 32 rows (smem)
+  // d <= 128: N = 256 MMAs (64 KB stages at d = 128); d <= 256: N = 128; d = 512: 32 rows (smem)
+  int tile_n = kblocks <= 2 ? 256 : (kblocks <= 4 ? 128 : 32);
   if (tile_n > tile_cap) tile_n = tile_cap;
   const int nq = (b->max_lq + 31) / 32;
   const int rep = nq == 3 ? 1 : 4 / nq;
@@ -1036,7 +1054,7 @@ static int prepare_tc(const cbx_batch* b, const void* d_rows, int64_t n_rows, fl
   p.doc_len = nullptr;
   p.n_tokens_dev = nullptr;
   p.ilv = 0;
-  p.k8 = 31 - __builtin_clz((unsigned)(tile_n / 8));  // d[k8] = 8-row boxes (tile_n >> k8 == 8)
+  p.k8 = std::min(4, 31 - __builtin_clz((unsigned)(tile_n / 8)));  // d[k8] = 8-row boxes (packed mode: tile_n <= 128)
   p.corpus_rows = n_rows;
   p.n_queries = b->n_queries;
   p.n_docs = b->n_docs;
