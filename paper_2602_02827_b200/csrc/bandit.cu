@@ -1,6 +1,6 @@
 // K2 — the Col-Bandit loop: host side of the C ABI (launch planning, sharded runs, mailboxes, IPC) and the
 // small non-template kernels. The loop kernel itself is in bandit_impl.cuh, instantiated per token dtype in
-// bandit_f16.cu / bandit_bf16.cu / bandit_f32.cu / bandit_f64.cu.
+// bandit_f16*.cu / bandit_bf16*.cu / bandit_f32.cu / bandit_f64.cu.
 #include "bandit_impl.cuh"
 
 namespace cbx {

@@ -1,8 +1,11 @@
-// K2 bandit kernels for __nv_bfloat16 tokens (see bandit_impl.cuh): one translation unit per dtype so the
+// K2 bandit kernels for __nv_bfloat16 tokens (see bandit_impl.cuh): the dispatchers, the warm-up pre-pass and the
+// layouts of rows above 512 bytes; the other layouts live in bandit_bf16_g16.cu and bandit_bf16_g8_g32.cu so the
 // instantiations compile in parallel. Built with -fmad=false like every bandit*.cu unit.
 #include "bandit_impl.cuh"
 
 namespace cbx {
+template int launch_bandit<__nv_bfloat16, 32, 2>(const BanditParams&, int64_t, size_t, cudaStream_t);
+template int launch_bandit<__nv_bfloat16, 32, 4>(const BanditParams&, int64_t, size_t, cudaStream_t);
 template int dispatch_bandit<__nv_bfloat16>(const BanditParams&, int64_t, size_t, cudaStream_t, int);
 template int dispatch_warm<__nv_bfloat16>(const BanditParams&, int, const int64_t*, unsigned, cudaStream_t);
 }  // namespace cbx

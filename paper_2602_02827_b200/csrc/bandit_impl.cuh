@@ -2240,7 +2240,7 @@ static void (*pick_bandit(bool wide, int sm, bool wreg))(const BanditParams) {
 }
 
 template <typename T, int G, int VPL>
-static int launch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, cudaStream_t st) {
+int launch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, cudaStream_t st) {
   // wide: every CTA has an SM to itself — because the runs fit one per SM, or because a run's shared-memory
   // state (pools of ~1600 rows and more) leaves no room for a second CTA anyway (cfg5: 2000 rows)
   const bool wide = CBX_BD_WIDE && (n_runs <= sm_count() || smem > 113 * 1024);
@@ -2271,6 +2271,17 @@ static int launch_bandit(const BanditParams& P, int64_t n_runs, size_t smem, cud
   CBX_LAUNCH_CHECK("bandit_kernel launch");
   return CBX_OK;
 }
+
+// The 16-bit layouts carry the most kernel variants (tensor-core screen, wide shapes, row cache): each group of
+// layouts is instantiated in its own translation unit (bandit_<dtype>*.cu) so the build runs them in parallel.
+#define CBX_BD_EXTERN_LAUNCH(T)                                                                       \
+  extern template int launch_bandit<T, 8, 1>(const BanditParams&, int64_t, size_t, cudaStream_t);    \
+  extern template int launch_bandit<T, 16, 1>(const BanditParams&, int64_t, size_t, cudaStream_t);   \
+  extern template int launch_bandit<T, 32, 1>(const BanditParams&, int64_t, size_t, cudaStream_t);   \
+  extern template int launch_bandit<T, 32, 2>(const BanditParams&, int64_t, size_t, cudaStream_t);   \
+  extern template int launch_bandit<T, 32, 4>(const BanditParams&, int64_t, size_t, cudaStream_t);
+CBX_BD_EXTERN_LAUNCH(__half)
+CBX_BD_EXTERN_LAUNCH(__nv_bfloat16)
 
 // lanes per token row: one 16-byte vector each, up to a warp; longer rows give lanes several vectors
 template <typename T>
@@ -2303,7 +2314,7 @@ int dispatch_warm(const BanditParams& P, int n_runs, const int64_t* wprefix, uns
   return fail(CBX_EINVAL, "bandit: embedding rows above 2 KiB are not supported");
 }
 
-// the kernel instantiations are compiled in one translation unit per token dtype (bandit_<dtype>.cu)
+// the kernel instantiations are compiled per token dtype (bandit_<dtype>.cu; the 16-bit layouts in three units each)
 extern template int dispatch_bandit<float>(const BanditParams&, int64_t, size_t, cudaStream_t, int);
 extern template int dispatch_bandit<__half>(const BanditParams&, int64_t, size_t, cudaStream_t, int);
 extern template int dispatch_bandit<__nv_bfloat16>(const BanditParams&, int64_t, size_t, cudaStream_t, int);

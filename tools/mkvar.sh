@@ -4,7 +4,7 @@
 set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
-srcs="bandit.cu bandit_f16.cu bandit_bf16.cu bandit_f32.cu bandit_f64.cu"
+srcs=$(cd paper_2602_02827_b200/csrc && ls bandit*.cu | tr "\n" " ")
 if [[ "$1" == *.cu ]]; then srcs=$1; shift; fi
 mkdir -p build/var_$name
 pids=""
